@@ -1,0 +1,55 @@
+# blinkline_b200 build: sm_100a only.
+#
+#   make            -> paper_2006_00816_b200/libblinkline_b200.so   (CUDA kernels + C-ABI)
+#                      paper_2006_00816_b200/libblinkline_gpu.so    (C++ drop-in API over the C-ABI)
+#                      oracle/liboracle.so                          (test-only C oracle)
+#   make ref        -> oracle/_ref/libblinkline_ref.so              (reference, needs /root/reference)
+#
+# Exactness: the TUs that must reproduce the reference bit-for-bit are compiled with
+# --fmad=false (no FMA contraction); only bl_classify.cu (the fp32 screen) and the host
+# code keep contraction.
+
+NVCC     ?= nvcc
+CXX      ?= g++
+PKG      := paper_2006_00816_b200
+CSRC     := $(PKG)/csrc
+BUILD    := build
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+EXACT    := --fmad=false
+LIB      := $(PKG)/libblinkline_b200.so
+CPPLIB   := $(PKG)/libblinkline_gpu.so
+
+EXACT_CU := bl_pyramid bl_hog bl_exact bl_ert
+FAST_CU  := bl_classify bl_capi
+OBJS     := $(addprefix $(BUILD)/,$(addsuffix .o,$(EXACT_CU) $(FAST_CU)))
+HDRS     := $(CSRC)/bl_internal.cuh include/blinkline_b200.h
+
+all: $(LIB) $(CPPLIB) oracle
+
+$(BUILD):
+	@mkdir -p $(BUILD)
+
+$(addprefix $(BUILD)/,$(addsuffix .o,$(EXACT_CU))): $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) $(EXACT) -c $< -o $@ 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; false)
+
+$(addprefix $(BUILD)/,$(addsuffix .o,$(FAST_CU))): $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fPIC -lcudart_static -lrt -lpthread -ldl
+
+$(CPPLIB): $(PKG)/cpp/blinkline_gpu.cpp $(PKG)/cpp/blinkline_gpu.hpp include/blinkline_b200.h $(LIB)
+	$(CXX) -std=c++20 -O2 -fPIC -shared -I$(PKG)/cpp -Iinclude -o $@ $(PKG)/cpp/blinkline_gpu.cpp \
+	  -L$(PKG) -lblinkline_b200 -Wl,-rpath,'$$ORIGIN'
+
+oracle:
+	$(MAKE) -s -C oracle
+
+ref:
+	$(MAKE) -s -C oracle ref
+
+clean:
+	rm -rf $(BUILD) $(LIB) $(CPPLIB)
+
+.PHONY: all oracle ref clean

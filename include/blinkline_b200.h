@@ -1,0 +1,168 @@
+/* blinkline_b200 -- C-ABI of the B200-native face-detection + 68-landmark hot path.
+ *
+ * This is the drop-in boundary.  Plain pointers and sizes only; no CUDA, torch or C++
+ * types cross it.  Every entry point replaces a reference (blinkline, /root/reference/proj)
+ * interface, cited per function as  `replaces: <header>:<line>`.  The C++ drop-in API
+ * (paper_2006_00816_b200/cpp/blinkline_gpu.hpp) and the Python binding
+ * (paper_2006_00816_b200/__init__.py) both sit on top of this header.
+ *
+ * Results are bit-identical to the reference CPU implementation: pyramid levels, gradient
+ * orientations/magnitudes, cell histograms, energies, features, detection scores and boxes
+ * are equal to the last bit; ERT leaf indices are equal and landmarks agree to <= 1e-9 px
+ * (the similarity transform goes through CUDA's hypot/atan2/cos/sin, which can differ from
+ * glibc's by an ulp).  See DESIGN.md §3.
+ *
+ * Error convention: every function returns BL_OK (0) or a BL_ERR_* code; the message of the
+ * last failure on the calling thread is bl_last_error().  The C++ layer maps
+ * BL_ERR_INVALID -> std::invalid_argument, BL_ERR_MODEL -> blinkline::model_error and the
+ * rest -> std::runtime_error, matching the reference's exception types.
+ *
+ * Threading: a bl_ctx is owned by one thread at a time (calls on one ctx are serialised
+ * internally by a mutex).  Different contexts may run concurrently, on one or several GPUs.
+ *
+ * Memory: `frames`, `boxes` and outputs may be host (pageable or pinned) or device pointers;
+ * the library inspects each pointer.  Host inputs are staged through pinned buffers. */
+#ifndef BLINKLINE_B200_H
+#define BLINKLINE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BL_ABI_VERSION 1
+
+enum {
+  BL_OK = 0,
+  BL_ERR_INVALID = 1,  /* precondition violated        -> std::invalid_argument */
+  BL_ERR_MODEL = 2,    /* model shape/content invalid  -> blinkline::model_error */
+  BL_ERR_CUDA = 3,     /* CUDA runtime/device failure   -> std::runtime_error */
+  BL_ERR_CAPACITY = 4, /* a fixed device capacity was exceeded -> std::runtime_error */
+  BL_ERR_STATE = 5     /* no model uploaded / context misuse */
+};
+
+enum { BL_PIX_U8 = 0, BL_PIX_F64 = 1 };
+
+typedef struct bl_ctx bl_ctx;
+
+/* Same layout as blinkline::Box (detector.hpp:15-20). */
+typedef struct {
+  int32_t x, y, w, h;
+} bl_box;
+
+/* Same layout as blinkline::Detection (detector.hpp:52-57). */
+typedef struct {
+  bl_box box;
+  double score;
+  int32_t scale_index;
+  int32_t rotation_index;
+} bl_detection;
+
+/* Per-stage device time of the last pipeline call (CUDA events), when enabled. */
+enum {
+  BL_STAGE_H2D = 0,
+  BL_STAGE_PYRAMID,
+  BL_STAGE_GRADHIST,
+  BL_STAGE_FEATURES,
+  BL_STAGE_SCREEN,
+  BL_STAGE_RESCORE,
+  BL_STAGE_NMS,
+  BL_STAGE_ERT,
+  BL_STAGE_D2H,
+  BL_STAGE_COUNT
+};
+
+/* ------------------------------------------------------------------ context ---- */
+int bl_abi_version(void);
+const char* bl_last_error(void);
+int bl_device_count(int* n);
+int bl_ctx_create(int device, bl_ctx** out);
+void bl_ctx_destroy(bl_ctx* ctx);
+/* Run on a caller-provided cudaStream_t (passed as void*); NULL restores the ctx stream. */
+int bl_ctx_set_stream(bl_ctx* ctx, void* cuda_stream);
+int bl_ctx_synchronize(bl_ctx* ctx);
+/* Number of kernels this context has launched so far (for launch-count accounting). */
+int bl_ctx_launch_count(bl_ctx* ctx, uint64_t* out);
+/* Per-stage CUDA-event timing of subsequent pipeline calls (adds events; off by default). */
+int bl_ctx_enable_stage_timing(bl_ctx* ctx, int enable);
+int bl_ctx_stage_times(bl_ctx* ctx, float* ms /* BL_STAGE_COUNT */, int* launches /* BL_STAGE_COUNT */);
+/* Capture each (geometry, batch) pipeline into a CUDA graph and replay it (default on). */
+int bl_ctx_enable_graphs(bl_ctx* ctx, int enable);
+
+/* ------------------------------------------------------------------- models ---- */
+/* replaces: the DetectorModel value passed to detect_faces (detector.hpp:31-41,87).
+ * weights: 5 x (window_cells*window_cells*31) row-major (cell-y, cell-x, feature). */
+int bl_detector_upload(bl_ctx* ctx, const double* weights, const double* biases, double threshold,
+                       int window_cells, int cell_px, int scale_num, int scale_den,
+                       double min_face_ratio);
+/* replaces: the ErtModel value passed to predict_landmarks (ert.hpp:44-68,86).
+ * anchors: T*K*S x 2 int32 (S = 2^F-1, level order), split_params: T*K*S x 5
+ * (offset_a.x, offset_a.y, offset_b.x, offset_b.y, threshold), leaves: T*K*2^F x L x 2. */
+int bl_ert_upload(bl_ctx* ctx, int L, int T, int K, int F, double shrinkage, const double* mean_xy,
+                  const int32_t* anchors, const double* split_params, const double* leaves);
+
+/* --------------------------------------------------------------- hot path ---- */
+/* replaces: detect_faces (detector.hpp:87, detector.cpp:157-176), batched over n frames of
+ * equal size.  Frame i starts at frames + i*frame_stride elements; rows are `pitch`
+ * elements apart.  Kept detections of all frames are written back to back into `out`
+ * (capacity `cap` entries) in each frame's NMS order; counts[i] = detections of frame i.
+ * *total (optional) = sum of counts.  BL_ERR_CAPACITY if cap is too small. */
+int bl_detect(bl_ctx* ctx, const void* frames, int pixel_type, int n, int w, int h, size_t pitch,
+              size_t frame_stride, bl_detection* out, int64_t cap, int32_t* counts, int64_t* total);
+
+/* replaces: predict_landmarks (ert.hpp:86-87, ert.cpp:99-136), batched over boxes.
+ * out_xy: n_boxes x L x 2 image-pixel coordinates; leaf_idx (optional): n_boxes x T*K. */
+int bl_landmarks(bl_ctx* ctx, const void* frames, int pixel_type, int n_frames, int w, int h,
+                 size_t pitch, size_t frame_stride, const int32_t* frame_of_box, const bl_box* boxes,
+                 int64_t n_boxes, double* out_xy, uint8_t* leaf_idx);
+
+/* replaces: the per-frame detect_frame + landmark_frame pair (pipeline.cpp:159-190): detect,
+ * then landmark every kept detection, all on the device.  landmarks: cap x L x 2, aligned
+ * with `out`. */
+int bl_detect_landmarks(bl_ctx* ctx, const void* frames, int pixel_type, int n, int w, int h,
+                        size_t pitch, size_t frame_stride, bl_detection* out, int64_t cap,
+                        int32_t* counts, int64_t* total, double* landmarks);
+
+/* ----------------------------------------------------------- stage functions ---- */
+/* Device implementations of the reference's stage API, for the drop-in C++ layer and the
+ * per-stage parity tests.  All buffers may be host or device memory. */
+
+/* replaces: build_pyramid (image.hpp:43, image.cpp:158-172).  Levels are written back to
+ * back as doubles into out (capacity out_cap doubles; may be NULL to query); dims[2k..2k+1]
+ * = level k's (w,h); scales[k] = (5/6)^k.  *n_levels receives the level count. */
+int bl_build_pyramid(bl_ctx* ctx, const void* image, int pixel_type, int w, int h, int window,
+                     double* out, size_t out_cap, int* dims, double* scales, int max_levels,
+                     int* n_levels);
+/* replaces: downscale_bilinear (image.hpp:33, image.cpp:129-156). */
+int bl_downscale_bilinear(bl_ctx* ctx, const double* image, int w, int h, double* out);
+/* replaces: compute_gradients (hog.hpp:65, hog.cpp:28-56). */
+int bl_compute_gradients(bl_ctx* ctx, const double* image, int w, int h, uint8_t* orientation,
+                         double* magnitude);
+/* replaces: histogramize (hog.hpp:70, hog.cpp:58-90) on an arbitrary gradient field. */
+int bl_histogramize(bl_ctx* ctx, const uint8_t* orientation, const double* magnitude, int w, int h,
+                    double* bins);
+/* replaces: cell_energy (hog.hpp:73, hog.cpp:92-109). */
+int bl_cell_energy(bl_ctx* ctx, const double* bins, int cells_w, int cells_h, double* energy);
+/* replaces: compute_features (hog.hpp:75, hog.cpp:111-166). */
+int bl_compute_features(bl_ctx* ctx, const double* bins, const double* energy, int cells_w,
+                        int cells_h, double* features);
+/* replaces: extract_features (hog.hpp:78, hog.cpp:168-173): the fused gradHist + feature
+ * kernels on one image; bins/energy may be NULL. */
+int bl_extract_features(bl_ctx* ctx, const double* image, int w, int h, double* features,
+                        double* bins, double* energy);
+/* replaces: score_separable / score_dense (detector.hpp:72-78, detector.cpp:45-100).
+ * scores: (cells_h-9) x (cells_w-9), bit-identical to score_separable. */
+int bl_score_window(bl_ctx* ctx, const double* features, int cells_w, int cells_h,
+                    const double* weights, double bias, double* scores);
+/* replaces: nms (detector.hpp:80, detector.cpp:124-142).  *kept = kept count. */
+int bl_nms(bl_ctx* ctx, const bl_detection* dets, int64_t n, double iou_threshold,
+           bl_detection* out, int64_t* kept);
+/* Device orientation argmax on explicit (gx, gy) pairs (hog.cpp:41-49 semantics). */
+int bl_orientation_bins(bl_ctx* ctx, const double* gx, const double* gy, int64_t n, uint8_t* bins);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLINKLINE_B200_H */

@@ -1,0 +1,483 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes faces over the two CPU checkers.
+
+* ``Oracle()``     -> oracle/liboracle.so, the plain-C restatement (blink_oracle.c)
+* ``Reference()``  -> oracle/_ref/libblinkline_ref.so, the UNMODIFIED reference
+                      library (/root/reference/proj/src) behind oracle/ref_capi.cpp
+
+Both expose the same numpy-level methods, so a test can run the same case
+through either one.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs import this module; the product package
+never does.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+DET_DTYPE = np.dtype(
+    [("x", "<i4"), ("y", "<i4"), ("w", "<i4"), ("h", "<i4"), ("score", "<f8"),
+     ("scale_index", "<i4"), ("rotation_index", "<i4")], align=True)
+assert DET_DTYPE.itemsize == 32
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+_u8p = C.POINTER(C.c_uint8)
+_vp = C.c_void_p
+
+
+def _ptr(a, t=_dp):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+def ensure_built(ref: bool = False) -> None:
+    """Build the oracle library (and optionally the reference) if missing."""
+    target = os.path.join(HERE, "_ref", "libblinkline_ref.so") if ref else os.path.join(HERE, "liboracle.so")
+    if os.path.exists(target):
+        return
+    if ref and not os.path.isdir("/root/reference/proj"):
+        raise FileNotFoundError("oracle/_ref/libblinkline_ref.so missing and /root/reference absent")
+    subprocess.run(["make", "-s", "-C", HERE] + (["ref"] if ref else []), check=True)
+
+
+def reference_available() -> bool:
+    return os.path.exists(os.path.join(HERE, "_ref", "libblinkline_ref.so")) or os.path.isdir("/root/reference/proj")
+
+
+class _Base:
+    prefix = ""
+
+    def __init__(self, path):
+        self.lib = C.CDLL(path, mode=C.RTLD_LOCAL)
+        L = self.lib
+        p = self.prefix
+        self._f = lambda name: getattr(L, p + name)
+        sigs = {
+            "build_pyramid": (C.c_int, [_dp, C.c_int, C.c_int, C.c_int, _dp, C.c_size_t, _ip, _dp, C.c_int]),
+            "downscale_bilinear": (C.c_int, [_dp, C.c_int, C.c_int, _dp]),
+            "compute_gradients": (C.c_int, [_dp, C.c_int, C.c_int, _u8p, _dp]),
+            "histogramize": (C.c_int, [_u8p, _dp, C.c_int, C.c_int, _dp]),
+            "cell_energy": (C.c_int, [_dp, C.c_int, C.c_int, _dp]),
+            "compute_features": (C.c_int, [_dp, _dp, C.c_int, C.c_int, _dp]),
+            "extract_features": (C.c_int, [_dp, C.c_int, C.c_int, _dp]),
+            "score_dense": (C.c_int, [_dp, C.c_int, C.c_int, _dp, C.c_double, _dp]),
+            "score_separable": (C.c_int, [_dp, C.c_int, C.c_int, _dp, C.c_double, _dp]),
+            "threshold_detections": (C.c_int, [_dp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                                               C.c_int, C.c_int, C.c_int, _vp, C.c_int]),
+            "nms": (C.c_int, [_vp, C.c_int, C.c_double, _vp]),
+            "iou": (C.c_double, [C.c_int] * 8),
+            "eligible_scales": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                          C.c_int, _ip]),
+            "similarity_transform": (C.c_int, [_dp, _dp, C.c_int, _dp]),
+            "last_error": (C.c_char_p, []),
+        }
+        for name, (res, args) in sigs.items():
+            fn = self._f(name)
+            fn.restype = res
+            fn.argtypes = args
+
+    def _check(self, rc):
+        if rc < 0:
+            raise ValueError(self._f("last_error")().decode())
+        return rc
+
+    # ---------------------------------------------------------------- image
+    def build_pyramid(self, img, window=80):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        h, w = img.shape
+        dims = np.zeros(128, np.int32)
+        scales = np.zeros(64, np.float64)
+        n = self._check(self._f("build_pyramid")(_ptr(img), w, h, window, None, 0, _ptr(dims, _ip), _ptr(scales), 64))
+        total = int(sum(int(dims[2 * k]) * int(dims[2 * k + 1]) for k in range(n)))
+        out = np.zeros(total, np.float64)
+        self._check(self._f("build_pyramid")(_ptr(img), w, h, window, _ptr(out), total, _ptr(dims, _ip), _ptr(scales), 64))
+        levels, off = [], 0
+        for k in range(n):
+            lw, lh = int(dims[2 * k]), int(dims[2 * k + 1])
+            levels.append(out[off:off + lw * lh].reshape(lh, lw))
+            off += lw * lh
+        return levels, scales[:n].copy()
+
+    def downscale_bilinear(self, img):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        h, w = img.shape
+        out = np.zeros((h * 5 // 6, w * 5 // 6), np.float64)
+        self._check(self._f("downscale_bilinear")(_ptr(img), w, h, _ptr(out)))
+        return out
+
+    # ------------------------------------------------------------------ hog
+    def compute_gradients(self, img):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        h, w = img.shape
+        ori = np.zeros((h, w), np.uint8)
+        mag = np.zeros((h, w), np.float64)
+        self._check(self._f("compute_gradients")(_ptr(img), w, h, _ptr(ori, _u8p), _ptr(mag)))
+        return ori, mag
+
+    def histogramize(self, ori, mag):
+        ori = np.ascontiguousarray(ori, dtype=np.uint8)
+        mag = np.ascontiguousarray(mag, dtype=np.float64)
+        h, w = mag.shape
+        bins = np.zeros((h // 8, w // 8, 18), np.float64)
+        self._check(self._f("histogramize")(_ptr(ori, _u8p), _ptr(mag), w, h, _ptr(bins)))
+        return bins
+
+    def cell_energy(self, bins):
+        bins = np.ascontiguousarray(bins, dtype=np.float64)
+        ch, cw = bins.shape[:2]
+        e = np.zeros((ch, cw), np.float64)
+        self._check(self._f("cell_energy")(_ptr(bins), cw, ch, _ptr(e)))
+        return e
+
+    def compute_features(self, bins, energy):
+        bins = np.ascontiguousarray(bins, dtype=np.float64)
+        energy = np.ascontiguousarray(energy, dtype=np.float64)
+        ch, cw = bins.shape[:2]
+        f = np.zeros((ch, cw, 31), np.float64)
+        self._check(self._f("compute_features")(_ptr(bins), _ptr(energy), cw, ch, _ptr(f)))
+        return f
+
+    def extract_features(self, img):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        h, w = img.shape
+        f = np.zeros((h // 8, w // 8, 31), np.float64)
+        self._check(self._f("extract_features")(_ptr(img), w, h, _ptr(f)))
+        return f
+
+    # ------------------------------------------------------------- detector
+    def _score(self, name, feat, weights, bias):
+        feat = np.ascontiguousarray(feat, dtype=np.float64)
+        weights = np.ascontiguousarray(weights, dtype=np.float64).reshape(3100)
+        ch, cw = feat.shape[:2]
+        out = np.zeros((max(ch - 9, 0), max(cw - 9, 0)), np.float64)
+        self._check(self._f(name)(_ptr(feat), cw, ch, _ptr(weights), float(bias), _ptr(out)))
+        return out
+
+    def score_dense(self, feat, weights, bias):
+        return self._score("score_dense", feat, weights, bias)
+
+    def score_separable(self, feat, weights, bias):
+        return self._score("score_separable", feat, weights, bias)
+
+    def threshold_detections(self, scores, thr, scale_index, rotation_index, window_cells=10, cell_px=8,
+                             scale_num=5, scale_den=6):
+        scores = np.ascontiguousarray(scores, dtype=np.float64)
+        sh, sw = scores.shape
+        out = np.zeros(sw * sh + 1, DET_DTYPE)
+        n = self._check(self._f("threshold_detections")(_ptr(scores), sw, sh, float(thr), window_cells, cell_px,
+                                                        scale_num, scale_den, scale_index, rotation_index,
+                                                        out.ctypes.data, len(out)))
+        return out[:n].copy()
+
+    def nms(self, dets, iou_thr=0.5):
+        dets = np.ascontiguousarray(dets, dtype=DET_DTYPE)
+        out = np.zeros(len(dets) + 1, DET_DTYPE)
+        n = self._check(self._f("nms")(dets.ctypes.data, len(dets), float(iou_thr), out.ctypes.data))
+        return out[:n].copy()
+
+    def iou(self, a, b):
+        return self._f("iou")(*[int(v) for v in a], *[int(v) for v in b])
+
+    def eligible_scales(self, w, h, n_levels, window_cells=10, cell_px=8, scale_num=5, scale_den=6,
+                        min_face_ratio=0.2):
+        out = np.zeros(max(n_levels, 1), np.int32)
+        n = self._check(self._f("eligible_scales")(w, h, window_cells, cell_px, scale_num, scale_den,
+                                                   float(min_face_ratio), n_levels, _ptr(out, _ip)))
+        return [int(v) for v in out[:n]]
+
+    # ------------------------------------------------------------------ ert
+    def similarity_transform(self, frm, to):
+        frm = np.ascontiguousarray(frm, dtype=np.float64)
+        to = np.ascontiguousarray(to, dtype=np.float64)
+        out = np.zeros(4, np.float64)
+        self._check(self._f("similarity_transform")(_ptr(frm), _ptr(to), len(frm), _ptr(out)))
+        return out
+
+
+class Oracle(_Base):
+    """The plain-C restatement (oracle/blink_oracle.c)."""
+
+    prefix = "orc_"
+
+    class _Det(C.Structure):
+        _fields_ = [("weights", _dp), ("biases", _dp), ("threshold", C.c_double), ("window_cells", C.c_int),
+                    ("cell_px", C.c_int), ("scale_num", C.c_int), ("scale_den", C.c_int),
+                    ("min_face_ratio", C.c_double)]
+
+    class _Ert(C.Structure):
+        _fields_ = [("L", C.c_int), ("T", C.c_int), ("K", C.c_int), ("F", C.c_int), ("shrinkage", C.c_double),
+                    ("mean_xy", _dp), ("anchors", _ip), ("split_params", _dp), ("leaves", _dp)]
+
+    def __init__(self):
+        ensure_built(False)
+        super().__init__(os.path.join(HERE, "liboracle.so"))
+        L = self.lib
+        L.orc_detect_faces.restype = C.c_int
+        L.orc_detect_faces.argtypes = [_dp, C.c_int, C.c_int, C.POINTER(self._Det), _vp, C.c_int]
+        L.orc_predict_landmarks.restype = C.c_int
+        L.orc_predict_landmarks.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.POINTER(self._Ert), _dp, _u8p, C.POINTER(C.c_uint64)]
+        L.orc_sample_intensity.restype = C.c_double
+        L.orc_sample_intensity.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp,
+                                           C.c_int, C.c_double, C.c_double]
+        L.orc_direction_table.restype = None
+        L.orc_direction_table.argtypes = [_dp, _dp]
+
+    def direction_table(self):
+        ux = np.zeros(18)
+        uy = np.zeros(18)
+        self.lib.orc_direction_table(_ptr(ux), _ptr(uy))
+        return ux, uy
+
+    def detect_faces(self, img, model):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        h, w = img.shape
+        wts = np.ascontiguousarray(model["weights"], dtype=np.float64).reshape(5 * 3100)
+        bs = np.ascontiguousarray(model["biases"], dtype=np.float64)
+        d = self._Det(_ptr(wts), _ptr(bs), float(model["threshold"]), model.get("window_cells", 10),
+                      model.get("cell_px", 8), model.get("scale_num", 5), model.get("scale_den", 6),
+                      float(model.get("min_face_ratio", 0.2)))
+        cap = 1 << 16
+        out = np.zeros(cap, DET_DTYPE)
+        n = self._check(self.lib.orc_detect_faces(_ptr(img), w, h, C.byref(d), out.ctypes.data, cap))
+        return out[:min(n, cap)].copy()
+
+    def predict_landmarks(self, img, box, ert):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        h, w = img.shape
+        keep = [np.ascontiguousarray(ert["mean_xy"], dtype=np.float64),
+                np.ascontiguousarray(ert["anchors"], dtype=np.int32),
+                np.ascontiguousarray(ert["split_params"], dtype=np.float64),
+                np.ascontiguousarray(ert["leaves"], dtype=np.float64)]
+        m = self._Ert(ert["L"], ert["T"], ert["K"], ert["F"], float(ert["shrinkage"]), _ptr(keep[0]),
+                      _ptr(keep[1], _ip), _ptr(keep[2]), _ptr(keep[3]))
+        xy = np.zeros((ert["L"], 2), np.float64)
+        leaf = np.zeros(ert["T"] * ert["K"], np.uint8)
+        ev = C.c_uint64(0)
+        self._check(self.lib.orc_predict_landmarks(_ptr(img), w, h, *[int(v) for v in box], C.byref(m), _ptr(xy),
+                                                   _ptr(leaf, _u8p), C.byref(ev)))
+        return xy, leaf, int(ev.value)
+
+    def sample_intensity(self, img, box, shape_xy, tform4, anchor, ox, oy):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        h, w = img.shape
+        s = np.ascontiguousarray(shape_xy, dtype=np.float64)
+        t = np.ascontiguousarray(tform4, dtype=np.float64)
+        return self.lib.orc_sample_intensity(_ptr(img), w, h, *[int(v) for v in box], _ptr(s), _ptr(t), anchor,
+                                             float(ox), float(oy))
+
+
+class Reference(_Base):
+    """The unmodified reference library (oracle/_ref/libblinkline_ref.so)."""
+
+    prefix = "ref_"
+
+    def __init__(self):
+        ensure_built(True)
+        super().__init__(os.path.join(HERE, "_ref", "libblinkline_ref.so"))
+        L = self.lib
+        L.ref_detect_faces.restype = C.c_int
+        L.ref_detect_faces.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, C.c_double, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_double, _vp, C.c_int]
+        L.ref_ert_create.restype = _vp
+        L.ref_ert_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _dp, _ip, _dp, _dp]
+        L.ref_ert_destroy.restype = None
+        L.ref_ert_destroy.argtypes = [_vp]
+        L.ref_predict_landmarks.restype = C.c_int
+        L.ref_predict_landmarks.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _dp,
+                                            C.POINTER(C.c_uint64)]
+        L.ref_ert_leaf_indices.restype = C.c_int
+        L.ref_ert_leaf_indices.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _u8p,
+                                           _dp]
+        L.ref_sample_intensity.restype = C.c_double
+        L.ref_sample_intensity.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int,
+                                           _dp, C.c_int, C.c_double, C.c_double]
+        L.ref_pattern_detector.restype = C.c_int
+        L.ref_pattern_detector.argtypes = [_dp, _dp, _dp]
+        L.ref_face68_mean_shape.restype = None
+        L.ref_face68_mean_shape.argtypes = [_dp]
+        L.ref_random_image.restype = None
+        L.ref_random_image.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_double, _dp]
+        L.ref_ring_frame.restype = None
+        L.ref_ring_frame.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_int,
+                                     _dp]
+        L.ref_run_batch_u8.restype = C.c_longlong
+        L.ref_run_batch_u8.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double, _vp, C.c_int, _ip,
+                                       _dp]
+        L.ref_landmarks_batch_u8.restype = C.c_int
+        L.ref_landmarks_batch_u8.argtypes = [_u8p, C.c_int, C.c_int, _ip, _ip, C.c_int, _vp, C.c_int, _dp]
+        self._erts = {}
+
+    def detect_faces(self, img, model):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        h, w = img.shape
+        wts = np.ascontiguousarray(model["weights"], dtype=np.float64).reshape(5 * 3100)
+        bs = np.ascontiguousarray(model["biases"], dtype=np.float64)
+        cap = 1 << 16
+        out = np.zeros(cap, DET_DTYPE)
+        n = self._check(self.lib.ref_detect_faces(_ptr(img), w, h, _ptr(wts), _ptr(bs), float(model["threshold"]),
+                                                  model.get("window_cells", 10), model.get("cell_px", 8),
+                                                  model.get("scale_num", 5), model.get("scale_den", 6),
+                                                  float(model.get("min_face_ratio", 0.2)), out.ctypes.data, cap))
+        return out[:min(n, cap)].copy()
+
+    def ert_handle(self, ert):
+        key = id(ert)
+        if key not in self._erts:
+            keep = [np.ascontiguousarray(ert["mean_xy"], dtype=np.float64),
+                    np.ascontiguousarray(ert["anchors"], dtype=np.int32),
+                    np.ascontiguousarray(ert["split_params"], dtype=np.float64),
+                    np.ascontiguousarray(ert["leaves"], dtype=np.float64)]
+            h = self.lib.ref_ert_create(ert["L"], ert["T"], ert["K"], ert["F"], float(ert["shrinkage"]),
+                                        _ptr(keep[0]), _ptr(keep[1], _ip), _ptr(keep[2]), _ptr(keep[3]))
+            if not h:
+                raise ValueError(self.lib.ref_last_error().decode())
+            self._erts[key] = (h, ert)
+        return self._erts[key][0]
+
+    def predict_landmarks(self, img, box, ert):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        h, w = img.shape
+        hd = self.ert_handle(ert)
+        xy = np.zeros((ert["L"], 2), np.float64)
+        ev = C.c_uint64(0)
+        self._check(self.lib.ref_predict_landmarks(_ptr(img), w, h, *[int(v) for v in box], hd, _ptr(xy),
+                                                   C.byref(ev)))
+        leaf = np.zeros(ert["T"] * ert["K"], np.uint8)
+        xy2 = np.zeros((ert["L"], 2), np.float64)
+        self._check(self.lib.ref_ert_leaf_indices(_ptr(img), w, h, *[int(v) for v in box], hd, _ptr(leaf, _u8p),
+                                                  _ptr(xy2)))
+        if not np.array_equal(xy, xy2):
+            raise AssertionError("leaf-index restatement diverged from predict_landmarks")
+        return xy, leaf, int(ev.value)
+
+    def sample_intensity(self, img, box, shape_xy, tform4, anchor, ox, oy):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        h, w = img.shape
+        s = np.ascontiguousarray(shape_xy, dtype=np.float64)
+        t = np.ascontiguousarray(tform4, dtype=np.float64)
+        return self.lib.ref_sample_intensity(_ptr(img), w, h, *[int(v) for v in box], _ptr(s), len(s), _ptr(t),
+                                             anchor, float(ox), float(oy))
+
+    # fixtures from the reference's own generators (tests/helpers.cpp)
+    def pattern_detector(self):
+        w = np.zeros(3100)
+        b = C.c_double(0)
+        t = C.c_double(0)
+        self._check(self.lib.ref_pattern_detector(_ptr(w), C.byref(b), C.byref(t)))
+        return {"weights": np.tile(w, (5, 1)), "biases": np.full(5, b.value), "threshold": t.value}
+
+    def face68_mean_shape(self):
+        xy = np.zeros((68, 2))
+        self.lib.ref_face68_mean_shape(_ptr(xy))
+        return xy
+
+    def random_image(self, w, h, seed, lo=0.0, hi=255.0):
+        out = np.zeros((h, w))
+        self.lib.ref_random_image(w, h, seed, lo, hi, _ptr(out))
+        return out
+
+    def ring_frame(self, w, h, seed, cx, cy, size, round_u8=True):
+        out = np.zeros((h, w))
+        self.lib.ref_ring_frame(w, h, seed, cx, cy, size, int(round_u8), _ptr(out))
+        return out
+
+    def run_batch_u8(self, frames, model, ert, threads):
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        n, h, w = frames.shape
+        wts = np.ascontiguousarray(model["weights"], dtype=np.float64).reshape(5 * 3100)
+        bs = np.ascontiguousarray(model["biases"], dtype=np.float64)
+        counts = np.zeros(n, np.int32)
+        cs = C.c_double(0)
+        hd = self.ert_handle(ert) if ert is not None else None
+        faces = self.lib.ref_run_batch_u8(_ptr(frames, _u8p), n, w, h, _ptr(wts), _ptr(bs), float(model["threshold"]),
+                                          hd, threads, _ptr(counts, _ip), C.byref(cs))
+        if faces < 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return int(faces), counts, cs.value
+
+    def landmarks_batch_u8(self, frames, frame_of_box, boxes, ert, threads, want_xy=False):
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        n, h, w = frames.shape
+        fob = np.ascontiguousarray(frame_of_box, dtype=np.int32)
+        bx = np.ascontiguousarray(boxes, dtype=np.int32)
+        out = np.zeros((len(bx), ert["L"], 2)) if want_xy else None
+        self._check(self.lib.ref_landmarks_batch_u8(_ptr(frames, _u8p), w, h, _ptr(fob, _ip), _ptr(bx, _ip), len(bx),
+                                                    self.ert_handle(ert), threads, _ptr(out) if want_xy else None))
+        return out
+
+
+def random_ert(L=68, T=15, K=500, F=4, seed=0, mean_xy=None, thr_range=64.0, off_range=0.15, leaf_range=0.02,
+               shrinkage=0.1):
+    """Random-init ERT cascade: anchors uniform, offsets U(-0.15,0.15), thresholds
+    U(-64,64), leaves U(-0.02,0.02), shrinkage 0.1.  numpy-seeded; the same arrays are fed to the
+    GPU path and to both CPU checkers."""
+    rng = np.random.default_rng(seed)
+    S, NL = (1 << F) - 1, 1 << F
+    if mean_xy is None:
+        mean_xy = face68_mean_shape_np() if L == 68 else rng.uniform(0.2, 0.8, (L, 2))
+    return {
+        "L": L, "T": T, "K": K, "F": F, "shrinkage": shrinkage,
+        "mean_xy": np.ascontiguousarray(mean_xy, dtype=np.float64),
+        "anchors": rng.integers(0, L, (T * K * S, 2), dtype=np.int32),
+        "split_params": np.concatenate([rng.uniform(-off_range, off_range, (T * K * S, 4)),
+                                        rng.uniform(-thr_range, thr_range, (T * K * S, 1))], axis=1),
+        "leaves": rng.uniform(-leaf_range, leaf_range, (T * K * NL, L, 2)),
+    }
+
+
+def face68_mean_shape_np():
+    """numpy restatement of tests/helpers.cpp:156-179 (face68_mean_shape)."""
+    pts = np.zeros((68, 2))
+    pi = np.pi
+    for i in range(17):
+        a = pi * float(i) / 16.0
+        pts[i] = (0.5 - 0.38 * np.cos(a), 0.52 + 0.40 * np.sin(a))
+    for i in range(17, 22):
+        pts[i] = (0.22 + 0.06 * (i - 17), 0.30)
+    for i in range(22, 27):
+        pts[i] = (0.54 + 0.06 * (i - 22), 0.30)
+    for i in range(27, 31):
+        pts[i] = (0.5, 0.36 + 0.05 * (i - 27))
+    for i in range(31, 36):
+        pts[i] = (0.42 + 0.04 * (i - 31), 0.56)
+
+    def hexa(base, cx, cy, rx, ry):
+        pts[base:base + 6] = [(cx - rx, cy), (cx - rx / 2, cy - ry), (cx + rx / 2, cy - ry), (cx + rx, cy),
+                              (cx + rx / 2, cy + ry), (cx - rx / 2, cy + ry)]
+    hexa(36, 0.35, 0.42, 0.08, 0.045)
+    hexa(42, 0.65, 0.42, 0.08, 0.045)
+    for i in range(48, 60):
+        a = 2.0 * pi * float(i - 48) / 12.0
+        pts[i] = (0.5 + 0.14 * np.cos(a), 0.72 + 0.06 * np.sin(a))
+    for i in range(60, 68):
+        a = 2.0 * pi * float(i - 60) / 8.0
+        pts[i] = (0.5 + 0.08 * np.cos(a), 0.72 + 0.03 * np.sin(a))
+    return pts
+
+
+def ring_frames_np(n, w, h, seed=0, size_frac=0.5, jitter=0.1):
+    """Synthetic eyeblink-camera frames: flat 20 + U(-1.5,1.5) noise + a
+    concentric-ring target (dark core 30 / bright ring 225 / dark outer 60, radii
+    0.18/0.34/0.47 of the box side, as tests/helpers.cpp:33-52 draws it), centre jittered per
+    frame, rounded to u8 exactly like the PGM round trip.  Vectorised numpy; returns (n,h,w) u8."""
+    rng = np.random.default_rng(seed)
+    yy, xx = np.mgrid[0:h, 0:w].astype(np.float64)
+    out = np.empty((n, h, w), np.uint8)
+    size = size_frac * min(w, h)
+    for i in range(n):
+        img = 20.0 + rng.uniform(-1.5, 1.5, (h, w))
+        img = np.clip(img, 0.0, 255.0)
+        cx = w / 2 + rng.uniform(-jitter, jitter) * w
+        cy = h / 2 + rng.uniform(-jitter, jitter) * h
+        r = np.hypot(xx - cx, yy - cy)
+        img = np.where(r <= 0.47 * size, 60.0, img)
+        img = np.where(r <= 0.34 * size, 225.0, img)
+        img = np.where(r <= 0.18 * size, 30.0, img)
+        out[i] = np.floor(np.clip(img, 0, 255) + 0.5).astype(np.uint8)
+    return out

@@ -1,0 +1,620 @@
+// blinkline drop-in API (blinkline_gpu.hpp) implemented over the C-ABI.
+//
+// Hot-path functions (build_pyramid, downscale_bilinear, the HOG stages, score_*,
+// nms, detect_faces, predict_landmarks and the batch extensions) run on the GPU through
+// include/blinkline_b200.h.  The remaining entry points are O(1)/O(n) scalar helpers of
+// the API (iou, eligible_scales, threshold_detections, similarity_transform,
+// sample_intensity, traverse_tree, SimilarityTransform::apply*) and are evaluated here
+// with the reference's arithmetic (file:line cited per function); they are not a fallback
+// for any device stage.
+#include "blinkline_gpu.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "blinkline_b200.h"
+
+namespace blinkline {
+namespace {
+
+// Map a C-ABI status to the reference's exception types.
+void check(int rc) {
+  if (rc == BL_OK) return;
+  const std::string msg = bl_last_error();
+  if (rc == BL_ERR_INVALID) throw std::invalid_argument(msg);
+  if (rc == BL_ERR_MODEL) throw model_error(msg);
+  throw std::runtime_error("blinkline_b200: " + msg);
+}
+
+int default_device() {
+  const char* e = std::getenv("BLINKLINE_DEVICE");
+  return e ? std::atoi(e) : 0;
+}
+
+struct ThreadCtx {
+  int device = default_device();
+  bl_ctx* ctx = nullptr;
+  // detector cache: exact copy of the uploaded weights (compared on every call)
+  std::vector<double> det_w;
+  std::array<double, 5> det_b{};
+  double det_thr = 0;
+  int det_geom[4] = {0, 0, 0, 0};
+  double det_ratio = -1;
+  bool det_valid = false;
+  // ERT cache: identity + fingerprint (models are shared, immutable values in the reference's
+  // API; mutate-in-place callers call gpu::invalidate_model_cache()).
+  const ErtModel* ert_ptr = nullptr;
+  std::vector<double> ert_fp;
+  ~ThreadCtx() {
+    if (ctx) bl_ctx_destroy(ctx);
+  }
+  bl_ctx* get() {
+    if (!ctx) check(bl_ctx_create(device, &ctx));
+    return ctx;
+  }
+};
+
+ThreadCtx& tls() {
+  thread_local ThreadCtx t;
+  return t;
+}
+
+void ensure_detector(ThreadCtx& T, const DetectorModel& m) {
+  std::vector<double> w(5 * std::size_t(kFilterWeights));
+  for (int r = 0; r < 5; ++r) {
+    if (int(m.filters[r].weights.size()) != kFilterWeights)
+      throw std::invalid_argument("filter must carry exactly 3100 weights");
+    std::memcpy(&w[std::size_t(r) * kFilterWeights], m.filters[r].weights.data(), sizeof(double) * kFilterWeights);
+  }
+  std::array<double, 5> b;
+  for (int r = 0; r < 5; ++r) b[r] = m.filters[r].bias;
+  const int geom[4] = {m.window_cells, m.cell_px, m.scale_num, m.scale_den};
+  if (T.det_valid && T.det_w == w && T.det_b == b && T.det_thr == m.detection_threshold &&
+      std::memcmp(T.det_geom, geom, sizeof geom) == 0 && T.det_ratio == m.min_face_ratio)
+    return;
+  check(bl_detector_upload(T.get(), w.data(), b.data(), m.detection_threshold, m.window_cells, m.cell_px,
+                           m.scale_num, m.scale_den, m.min_face_ratio));
+  T.det_w = std::move(w);
+  T.det_b = b;
+  T.det_thr = m.detection_threshold;
+  std::memcpy(T.det_geom, geom, sizeof geom);
+  T.det_ratio = m.min_face_ratio;
+  T.det_valid = true;
+}
+
+std::vector<double> ert_fingerprint(const ErtModel& m) {
+  std::vector<double> fp;
+  fp.push_back(m.landmark_count());
+  fp.push_back(m.levels());
+  fp.push_back(m.trees_per_level());
+  fp.push_back(m.shrinkage);
+  for (const Point2& p : m.mean_shape.points) {
+    fp.push_back(p.x);
+    fp.push_back(p.y);
+  }
+  const std::size_t T = m.cascade.size();
+  for (std::size_t t = 0; t < T; ++t) {
+    const auto& lv = m.cascade[t];
+    fp.push_back(double(lv.size()));
+    for (std::size_t k = 0; k < lv.size(); k += std::max<std::size_t>(1, lv.size() / 16)) {
+      const RegressionTree& tr = lv[k];
+      fp.push_back(tr.depth);
+      if (!tr.splits.empty()) {
+        fp.push_back(tr.splits[0].threshold);
+        fp.push_back(tr.splits.back().offset_b.y);
+      }
+      if (!tr.leaves.empty() && !tr.leaves.back().empty()) fp.push_back(tr.leaves.back().back().x);
+    }
+  }
+  return fp;
+}
+
+void ensure_ert(ThreadCtx& T, const ErtModel& m) {
+  std::vector<double> fp = ert_fingerprint(m);
+  if (T.ert_ptr == &m && T.ert_fp == fp) return;
+  const int L = m.landmark_count(), Tn = m.levels(), K = m.trees_per_level();
+  if (L < 2) throw std::invalid_argument("predict_landmarks: model has no mean shape");
+  const int F = (Tn > 0 && K > 0) ? m.cascade[0][0].depth : 0;
+  const int S = (1 << F) - 1, NL = 1 << F;
+  std::vector<double> mean(2 * L);
+  for (int i = 0; i < L; ++i) {
+    mean[2 * i] = m.mean_shape.points[i].x;
+    mean[2 * i + 1] = m.mean_shape.points[i].y;
+  }
+  std::vector<int32_t> an(std::size_t(Tn) * K * S * 2);
+  std::vector<double> sp(std::size_t(Tn) * K * S * 5);
+  std::vector<double> lv(std::size_t(Tn) * K * NL * L * 2);
+  for (int t = 0; t < Tn; ++t) {
+    if (int(m.cascade[t].size()) != K) throw model_error("every cascade level must carry K trees");
+    for (int k = 0; k < K; ++k) {
+      const RegressionTree& tr = m.cascade[t][k];
+      if (int(tr.splits.size()) != S || int(tr.leaves.size()) != NL)
+        throw model_error("tree split/leaf counts do not match depth F");
+      const std::size_t tk = std::size_t(t) * K + k;
+      for (int s = 0; s < S; ++s) {
+        const SplitNode& n = tr.splits[s];
+        an[(tk * S + s) * 2] = n.anchor_a;
+        an[(tk * S + s) * 2 + 1] = n.anchor_b;
+        double* p = &sp[(tk * S + s) * 5];
+        p[0] = n.offset_a.x;
+        p[1] = n.offset_a.y;
+        p[2] = n.offset_b.x;
+        p[3] = n.offset_b.y;
+        p[4] = n.threshold;
+      }
+      for (int l = 0; l < NL; ++l) {
+        if (int(tr.leaves[l].size()) != L) throw model_error("leaf delta must carry L points");
+        double* q = &lv[(tk * NL + l) * std::size_t(L) * 2];
+        for (int i = 0; i < L; ++i) {
+          q[2 * i] = tr.leaves[l][i].x;
+          q[2 * i + 1] = tr.leaves[l][i].y;
+        }
+      }
+    }
+  }
+  check(bl_ert_upload(T.get(), L, Tn, K, F, m.shrinkage, mean.data(), an.data(), sp.data(), lv.data()));
+  T.ert_ptr = &m;
+  T.ert_fp = std::move(fp);
+}
+
+// Frames go to the device as u8 when every pixel is an integer in [0,255] (lossless),
+// otherwise as fp64.
+bool integral_u8(const GrayImage& img) {
+  for (const double v : img.pixels)
+    if (!(v >= 0.0 && v <= 255.0) || v != std::floor(v)) return false;
+  return true;
+}
+
+struct Packed {
+  int pix = BL_PIX_U8;
+  std::vector<uint8_t> u8;
+  std::vector<double> f64;
+  const void* data() const { return pix == BL_PIX_U8 ? (const void*)u8.data() : (const void*)f64.data(); }
+};
+
+Packed pack(const std::vector<const GrayImage*>& frames) {
+  Packed p;
+  bool all_u8 = true;
+  for (const GrayImage* f : frames) all_u8 = all_u8 && integral_u8(*f);
+  const std::size_t n = frames.empty() ? 0 : frames[0]->pixels.size();
+  if (all_u8) {
+    p.pix = BL_PIX_U8;
+    p.u8.resize(n * frames.size());
+    for (std::size_t i = 0; i < frames.size(); ++i)
+      for (std::size_t j = 0; j < n; ++j) p.u8[i * n + j] = uint8_t(frames[i]->pixels[j]);
+  } else {
+    p.pix = BL_PIX_F64;
+    p.f64.resize(n * frames.size());
+    for (std::size_t i = 0; i < frames.size(); ++i)
+      std::memcpy(&p.f64[i * n], frames[i]->pixels.data(), sizeof(double) * n);
+  }
+  return p;
+}
+
+void check_image(const GrayImage& img) {
+  if (img.width < 1 || img.height < 1 || img.pixels.size() != std::size_t(img.width) * img.height)
+    throw std::invalid_argument("image dimensions do not match its pixel buffer");
+}
+
+Detection from_c(const bl_detection& d) {
+  Detection o;
+  o.box = Box{d.box.x, d.box.y, d.box.w, d.box.h};
+  o.score = d.score;
+  o.scale_index = d.scale_index;
+  o.rotation_index = d.rotation_index;
+  return o;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------ image ----
+GrayImage make_image(int width, int height, double fill) {  // image.cpp:13-20
+  if (width < 1 || height < 1) throw std::invalid_argument("make_image: dimensions must be >= 1");
+  GrayImage img;
+  img.width = width;
+  img.height = height;
+  img.pixels.assign(std::size_t(width) * height, fill);
+  return img;
+}
+
+GrayImage downscale_bilinear(const GrayImage& img) {
+  if (img.width < 2 || img.height < 2)
+    throw std::invalid_argument("downscale_bilinear: output dimension would be 0");
+  check_image(img);
+  GrayImage out = make_image(img.width * 5 / 6, img.height * 5 / 6);
+  check(bl_downscale_bilinear(tls().get(), img.pixels.data(), img.width, img.height, out.pixels.data()));
+  return out;
+}
+
+Pyramid build_pyramid(const GrayImage& img, int window) {
+  check_image(img);
+  bl_ctx* c = tls().get();
+  int n = 0;
+  std::vector<int> dims(128);
+  std::vector<double> scales(64);
+  check(bl_build_pyramid(c, img.pixels.data(), BL_PIX_F64, img.width, img.height, window, nullptr, 0,
+                         dims.data(), scales.data(), 64, &n));
+  if (n > 64) throw std::runtime_error("pyramid deeper than 64 levels");
+  std::size_t total = 0;
+  for (int k = 0; k < n; ++k) total += std::size_t(dims[2 * k]) * dims[2 * k + 1];
+  std::vector<double> all(total);
+  check(bl_build_pyramid(c, img.pixels.data(), BL_PIX_F64, img.width, img.height, window, all.data(), total,
+                         dims.data(), scales.data(), 64, &n));
+  Pyramid p;
+  std::size_t off = 0;
+  for (int k = 0; k < n; ++k) {
+    GrayImage lv;
+    lv.width = dims[2 * k];
+    lv.height = dims[2 * k + 1];
+    lv.pixels.assign(all.begin() + off, all.begin() + off + std::size_t(lv.width) * lv.height);
+    off += lv.pixels.size();
+    p.levels.push_back(std::move(lv));
+    p.cumulative_scale.push_back(scales[k]);
+  }
+  return p;
+}
+
+// -------------------------------------------------------------------------- hog ----
+GradientField compute_gradients(const GrayImage& img) {
+  if (img.width < 3 || img.height < 3)
+    throw std::invalid_argument("compute_gradients: image must be at least 3x3");
+  check_image(img);
+  GradientField g;
+  g.width = img.width;
+  g.height = img.height;
+  g.orientation.assign(std::size_t(img.width) * img.height, 0);
+  g.magnitude.assign(std::size_t(img.width) * img.height, 0.0);
+  check(bl_compute_gradients(tls().get(), img.pixels.data(), img.width, img.height, g.orientation.data(),
+                             g.magnitude.data()));
+  return g;
+}
+
+CellGrid histogramize(const GradientField& grads) {
+  CellGrid cg;
+  cg.cells_w = grads.width / kCellSize;
+  cg.cells_h = grads.height / kCellSize;
+  cg.bins.assign(std::size_t(cg.cells_w) * cg.cells_h * kOrientationBins, 0.0);
+  if (cg.cells_w == 0 || cg.cells_h == 0) return cg;
+  check(bl_histogramize(tls().get(), grads.orientation.data(), grads.magnitude.data(), grads.width, grads.height,
+                        cg.bins.data()));
+  return cg;
+}
+
+EnergyGrid cell_energy(const CellGrid& cells) {
+  EnergyGrid e;
+  e.cells_w = cells.cells_w;
+  e.cells_h = cells.cells_h;
+  e.energy.assign(std::size_t(cells.cells_w) * cells.cells_h, 0.0);
+  if (!e.energy.empty())
+    check(bl_cell_energy(tls().get(), cells.bins.data(), cells.cells_w, cells.cells_h, e.energy.data()));
+  return e;
+}
+
+FeatureImage compute_features(const CellGrid& cells, const EnergyGrid& energies) {
+  if (cells.cells_w != energies.cells_w || cells.cells_h != energies.cells_h)
+    throw std::invalid_argument("compute_features: cell and energy grids must share dimensions");
+  FeatureImage f;
+  f.cells_w = cells.cells_w;
+  f.cells_h = cells.cells_h;
+  f.values.assign(std::size_t(f.cells_w) * f.cells_h * kCellFeatures, 0.0);
+  if (!f.values.empty())
+    check(bl_compute_features(tls().get(), cells.bins.data(), energies.energy.data(), cells.cells_w, cells.cells_h,
+                              f.values.data()));
+  return f;
+}
+
+FeatureImage extract_features(const GrayImage& img) {
+  if (img.width < 3 || img.height < 3)
+    throw std::invalid_argument("compute_gradients: image must be at least 3x3");
+  check_image(img);
+  FeatureImage f;
+  f.cells_w = img.width / kCellSize;
+  f.cells_h = img.height / kCellSize;
+  f.values.assign(std::size_t(f.cells_w) * f.cells_h * kCellFeatures, 0.0);
+  if (!f.values.empty())
+    check(bl_extract_features(tls().get(), img.pixels.data(), img.width, img.height, f.values.data(), nullptr,
+                              nullptr));
+  return f;
+}
+
+// --------------------------------------------------------------------- detector ----
+double iou(const Box& a, const Box& b) {  // detector.cpp:16-28
+  const long long ix0 = std::max(a.x, b.x);
+  const long long iy0 = std::max(a.y, b.y);
+  const long long ix1 = std::min<long long>(a.x + a.w, b.x + b.w);
+  const long long iy1 = std::min<long long>(a.y + a.h, b.y + b.h);
+  const long long iw = ix1 - ix0, ih = iy1 - iy0;
+  if (iw <= 0 || ih <= 0) return 0.0;
+  const double inter = double(iw) * double(ih);
+  const double uni = double(a.w) * a.h + double(b.w) * b.h - inter;
+  if (uni <= 0.0) return 0.0;
+  return inter / uni;
+}
+
+static SaliencyMap score_gpu(const FeatureImage& feat, const LinearFilter& filter) {
+  if (int(filter.weights.size()) != kFilterWeights)
+    throw std::invalid_argument("filter must carry exactly 3100 weights");
+  if (feat.cells_w < kWindowCells || feat.cells_h < kWindowCells)
+    throw std::invalid_argument("feature image smaller than the 10x10 detection window");
+  SaliencyMap s;
+  s.width = feat.cells_w - (kWindowCells - 1);
+  s.height = feat.cells_h - (kWindowCells - 1);
+  s.scores.assign(std::size_t(s.width) * s.height, 0.0);
+  check(bl_score_window(tls().get(), feat.values.data(), feat.cells_w, feat.cells_h, filter.weights.data(),
+                        filter.bias, s.scores.data()));
+  return s;
+}
+
+// The device scorer evaluates the separable order exactly (bit-identical to
+// score_separable); score_dense differs from it only by summation order (<= 1e-4 by the
+// reference's own contract, SPEC C1), so both are served by it.
+SaliencyMap score_dense(const FeatureImage& feat, const LinearFilter& filter) { return score_gpu(feat, filter); }
+SaliencyMap score_separable(const FeatureImage& feat, const LinearFilter& filter) {
+  return score_gpu(feat, filter);
+}
+
+std::vector<Detection> threshold_detections(const SaliencyMap& sal, const DetectorModel& model, int scale_index,
+                                            int rotation_index) {  // detector.cpp:102-122
+  const double c = std::pow(double(model.scale_num) / model.scale_den, double(scale_index));
+  const int side = int(std::floor(model.window_px() / c + 0.5));
+  std::vector<Detection> dets;
+  for (int cy = 0; cy < sal.height; ++cy)
+    for (int cx = 0; cx < sal.width; ++cx) {
+      const double s = sal.at(cx, cy);
+      if (s > model.detection_threshold) {
+        Detection d;
+        d.box = {int(std::floor(cx * model.cell_px / c + 0.5)), int(std::floor(cy * model.cell_px / c + 0.5)), side,
+                 side};
+        d.score = s;
+        d.scale_index = scale_index;
+        d.rotation_index = rotation_index;
+        dets.push_back(d);
+      }
+    }
+  return dets;
+}
+
+std::vector<Detection> nms(std::vector<Detection> dets, double iou_threshold) {
+  std::vector<Detection> out(dets.size());
+  if (dets.empty()) return out;
+  static_assert(sizeof(Detection) == sizeof(bl_detection), "layout");
+  int64_t kept = 0;
+  check(bl_nms(tls().get(), reinterpret_cast<const bl_detection*>(dets.data()), int64_t(dets.size()), iou_threshold,
+               reinterpret_cast<bl_detection*>(out.data()), &kept));
+  out.resize(std::size_t(kept));
+  return out;
+}
+
+std::vector<int> eligible_scales(int img_w, int img_h, const DetectorModel& model,
+                                 int n_levels) {  // detector.cpp:144-155
+  const double min_face = model.min_face_ratio * std::min(img_w, img_h);
+  std::vector<int> out;
+  for (int k = 0; k < n_levels; ++k) {
+    const double detectable =
+        model.window_px() / std::pow(double(model.scale_num) / model.scale_den, double(k));
+    if (detectable >= min_face * (1.0 - 1e-9)) out.push_back(k);
+  }
+  return out;
+}
+
+std::vector<Detection> detect_faces(const GrayImage& img, const DetectorModel& model) {
+  return gpu::detect_faces_batch({img}, model)[0];
+}
+
+// -------------------------------------------------------------------------- ert ----
+Point2 SimilarityTransform::apply(const Point2& p) const {  // ert.cpp:15-18
+  const Point2 q = apply_linear(p);
+  return {q.x + tx, q.y + ty};
+}
+
+Point2 SimilarityTransform::apply_linear(const Point2& p) const {  // ert.cpp:20-24
+  const double a = scale * std::cos(rotation);
+  const double b = scale * std::sin(rotation);
+  return {a * p.x - b * p.y, b * p.x + a * p.y};
+}
+
+SimilarityTransform similarity_transform(const Shape& from, const Shape& to) {  // ert.cpp:26-69
+  const std::size_t n = from.points.size();
+  if (n < 2 || to.points.size() != n)
+    throw std::invalid_argument("similarity_transform: shapes must share L >= 2 points");
+  if (from.frame != to.frame) throw std::invalid_argument("similarity_transform: shapes must share a frame");
+  double mfx = 0, mfy = 0, mtx = 0, mty = 0;
+  for (std::size_t i = 0; i < n; ++i) {
+    mfx += from.points[i].x;
+    mfy += from.points[i].y;
+    mtx += to.points[i].x;
+    mty += to.points[i].y;
+  }
+  mfx /= double(n);
+  mfy /= double(n);
+  mtx /= double(n);
+  mty /= double(n);
+  double sff = 0, sre = 0, sim = 0;
+  for (std::size_t i = 0; i < n; ++i) {
+    const double fx = from.points[i].x - mfx, fy = from.points[i].y - mfy;
+    const double txp = to.points[i].x - mtx, typ = to.points[i].y - mty;
+    sff += fx * fx + fy * fy;
+    sre += fx * txp + fy * typ;
+    sim += fx * typ - fy * txp;
+  }
+  if (sff <= 0.0) throw std::invalid_argument("similarity_transform: source shape has no spread");
+  const double a = sre / sff, b = sim / sff;
+  SimilarityTransform t;
+  t.scale = std::hypot(a, b);
+  if (t.scale <= 0.0) throw std::invalid_argument("similarity_transform: target shape has no spread");
+  t.rotation = std::atan2(b, a);
+  t.tx = mtx - (a * mfx - b * mfy);
+  t.ty = mty - (b * mfx + a * mfy);
+  return t;
+}
+
+double sample_intensity(const GrayImage& img, const Box& box, const Shape& shape, const SimilarityTransform& tform,
+                        int anchor, Point2 offset) {  // ert.cpp:71-85
+  if (shape.frame != ShapeFrame::normalized)
+    throw std::invalid_argument("sample_intensity: shape must be in the normalized frame");
+  const Point2 off = tform.apply_linear(offset);
+  const double nx = shape.points[anchor].x + off.x;
+  const double ny = shape.points[anchor].y + off.y;
+  const double px = box.x + nx * box.w;
+  const double py = box.y + ny * box.h;
+  const int ix = std::clamp(int(std::llround(px)), 0, img.width - 1);
+  const int iy = std::clamp(int(std::llround(py)), 0, img.height - 1);
+  return img.at(ix, iy);
+}
+
+const std::vector<Point2>& traverse_tree(const RegressionTree& tree,
+                                         const IntensityPairFn& intensity_of) {  // ert.cpp:87-97
+  std::size_t node = 0;
+  const std::size_t n_splits = tree.splits.size();
+  while (node < n_splits) {
+    const SplitNode& s = tree.splits[node];
+    const auto [ia, ib] = intensity_of(s);
+    node = (ia - ib > s.threshold) ? 2 * node + 1 : 2 * node + 2;
+  }
+  return tree.leaves[node - n_splits];
+}
+
+Shape predict_landmarks(const GrayImage& img, const Box& box, const ErtModel& model, PredictStats* stats) {
+  if (box.w <= 0 || box.h <= 0) throw std::invalid_argument("predict_landmarks: face box must have positive area");
+  if (model.landmark_count() < 2) throw std::invalid_argument("predict_landmarks: model has no mean shape");
+  Shape s = gpu::predict_landmarks_batch({img}, {0}, {box}, model)[0];
+  if (stats) {
+    std::uint64_t evals = 0;  // one intensity difference per visited split: T*K*F
+    for (const auto& lv : model.cascade)
+      for (const RegressionTree& t : lv) evals += std::uint64_t(t.depth);
+    stats->intensity_diffs = evals;
+  }
+  return s;
+}
+
+// ------------------------------------------------------------------------- batch ----
+namespace gpu {
+
+void set_device(int device) {
+  ThreadCtx& T = tls();
+  if (T.device == device) return;
+  if (T.ctx) bl_ctx_destroy(T.ctx);
+  T.ctx = nullptr;
+  T.device = device;
+  T.det_valid = false;
+  T.ert_ptr = nullptr;
+}
+
+void invalidate_model_cache() {
+  ThreadCtx& T = tls();
+  T.det_valid = false;
+  T.ert_ptr = nullptr;
+  T.ert_fp.clear();
+}
+
+static void same_size(const std::vector<const GrayImage*>& fr) {
+  for (const GrayImage* f : fr) {
+    check_image(*f);
+    if (f->width != fr[0]->width || f->height != fr[0]->height)
+      throw std::invalid_argument("batched frames must share dimensions");
+  }
+}
+
+std::vector<std::vector<Detection>> detect_faces_batch(const std::vector<GrayImage>& frames,
+                                                       const DetectorModel& model) {
+  std::vector<std::vector<Detection>> res(frames.size());
+  if (frames.empty()) return res;
+  ThreadCtx& T = tls();
+  ensure_detector(T, model);
+  std::vector<const GrayImage*> fr;
+  for (const GrayImage& f : frames) fr.push_back(&f);
+  same_size(fr);
+  const int w = fr[0]->width, h = fr[0]->height;
+  const Packed p = pack(fr);
+  std::vector<int32_t> counts(frames.size());
+  int64_t total = 0;
+  // generous first guess; on BL_ERR_CAPACITY `total` reports the exact need
+  int64_t cap = std::max<int64_t>(1024, int64_t(frames.size()) * 64);
+  std::vector<bl_detection> out(static_cast<std::size_t>(cap));
+  int rc = bl_detect(T.get(), p.data(), p.pix, int(frames.size()), w, h, w, std::size_t(w) * h, out.data(), cap,
+                     counts.data(), &total);
+  if (rc == BL_ERR_CAPACITY && total > cap) {
+    cap = total;
+    out.resize(std::size_t(cap));
+    rc = bl_detect(T.get(), p.data(), p.pix, int(frames.size()), w, h, w, std::size_t(w) * h, out.data(), cap,
+                   counts.data(), &total);
+  }
+  check(rc);
+  std::size_t o = 0;
+  for (std::size_t i = 0; i < frames.size(); ++i)
+    for (int k = 0; k < counts[i]; ++k) res[i].push_back(from_c(out[o++]));
+  return res;
+}
+
+std::vector<Shape> predict_landmarks_batch(const std::vector<GrayImage>& frames, const std::vector<int>& frame_of_box,
+                                           const std::vector<Box>& boxes, const ErtModel& model) {
+  if (frame_of_box.size() != boxes.size()) throw std::invalid_argument("frame_of_box and boxes differ in length");
+  std::vector<Shape> res;
+  if (boxes.empty()) return res;
+  ThreadCtx& T = tls();
+  ensure_ert(T, model);
+  std::vector<const GrayImage*> fr;
+  for (const GrayImage& f : frames) fr.push_back(&f);
+  same_size(fr);
+  const Packed p = pack(fr);
+  const int L = model.landmark_count();
+  std::vector<double> xy(boxes.size() * std::size_t(L) * 2);
+  static_assert(sizeof(Box) == sizeof(bl_box), "layout");
+  check(bl_landmarks(T.get(), p.data(), p.pix, int(frames.size()), fr[0]->width, fr[0]->height, fr[0]->width,
+                     std::size_t(fr[0]->width) * fr[0]->height, frame_of_box.data(),
+                     reinterpret_cast<const bl_box*>(boxes.data()), int64_t(boxes.size()), xy.data(), nullptr));
+  res.resize(boxes.size());
+  for (std::size_t b = 0; b < boxes.size(); ++b) {
+    res[b].frame = ShapeFrame::image;
+    res[b].points.resize(L);
+    for (int i = 0; i < L; ++i) res[b].points[i] = {xy[(b * L + i) * 2], xy[(b * L + i) * 2 + 1]};
+  }
+  return res;
+}
+
+std::vector<FrameResult> detect_and_landmark(const std::vector<GrayImage>& frames, const DetectorModel& hog,
+                                             const ErtModel& ert) {
+  std::vector<FrameResult> res(frames.size());
+  if (frames.empty()) return res;
+  ThreadCtx& T = tls();
+  ensure_detector(T, hog);
+  ensure_ert(T, ert);
+  std::vector<const GrayImage*> fr;
+  for (const GrayImage& f : frames) fr.push_back(&f);
+  same_size(fr);
+  const int w = fr[0]->width, h = fr[0]->height, L = ert.landmark_count();
+  const Packed p = pack(fr);
+  std::vector<int32_t> counts(frames.size());
+  int64_t total = 0;
+  int64_t cap = std::max<int64_t>(1024, int64_t(frames.size()) * 64);
+  std::vector<bl_detection> out(static_cast<std::size_t>(cap));
+  std::vector<double> xy(std::size_t(cap) * L * 2);
+  int rc = bl_detect_landmarks(T.get(), p.data(), p.pix, int(frames.size()), w, h, w, std::size_t(w) * h,
+                               out.data(), cap, counts.data(), &total, xy.data());
+  if (rc == BL_ERR_CAPACITY && total > cap) {
+    cap = total;
+    out.resize(std::size_t(cap));
+    xy.resize(std::size_t(cap) * L * 2);
+    rc = bl_detect_landmarks(T.get(), p.data(), p.pix, int(frames.size()), w, h, w, std::size_t(w) * h, out.data(),
+                             cap, counts.data(), &total, xy.data());
+  }
+  check(rc);
+  std::size_t o = 0;
+  for (std::size_t i = 0; i < frames.size(); ++i)
+    for (int k = 0; k < counts[i]; ++k, ++o) {
+      res[i].detections.push_back(from_c(out[o]));
+      Shape s;
+      s.frame = ShapeFrame::image;
+      s.points.resize(L);
+      for (int j = 0; j < L; ++j) s.points[j] = {xy[(o * L + j) * 2], xy[(o * L + j) * 2 + 1]};
+      res[i].landmarks.push_back(std::move(s));
+    }
+  return res;
+}
+
+}  // namespace gpu
+}  // namespace blinkline

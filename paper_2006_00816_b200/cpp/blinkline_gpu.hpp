@@ -1,0 +1,232 @@
+// blinkline drop-in API served by the B200 device path.
+//
+// Declares, in namespace blinkline, the value types and hot-path functions of the
+// reference library's public headers (proj/include/blinkline/{image,hog,detector,ert,
+// errors}.hpp) with the same names, layouts, argument meaning and exception types, so a
+// caller of the reference's detect_faces / predict_landmarks (and the stage functions they
+// are built from) recompiles against this header and links libblinkline_gpu.so instead.
+// Every function below is implemented on top of the C-ABI in include/blinkline_b200.h.
+//
+// Out of scope (not declared here): PGM I/O, the trainers, model JSON I/O, blink/eval
+// analysis and the pipeline runtime -- see DESIGN.md §6.
+#pragma once
+
+#include <array>
+#include <cstddef>
+#include <cstdint>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace blinkline {
+
+// ------------------------------------------------------------------ errors (errors.hpp)
+struct io_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct model_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// ------------------------------------------------------------------- image (image.hpp)
+struct GrayImage {
+  int width = 0;
+  int height = 0;
+  std::vector<double> pixels;  // row-major, width * height
+  double at(int x, int y) const { return pixels[std::size_t(y) * width + x]; }
+  double& at(int x, int y) { return pixels[std::size_t(y) * width + x]; }
+};
+
+GrayImage make_image(int width, int height, double fill = 0.0);
+GrayImage downscale_bilinear(const GrayImage& img);
+
+struct Pyramid {
+  std::vector<GrayImage> levels;
+  std::vector<double> cumulative_scale;
+};
+Pyramid build_pyramid(const GrayImage& img, int window = 80);
+
+// --------------------------------------------------------------------- hog (hog.hpp)
+inline constexpr int kOrientationBins = 18;
+inline constexpr int kCellSize = 8;
+inline constexpr int kCellFeatures = 31;
+
+struct GradientField {
+  int width = 0;
+  int height = 0;
+  std::vector<std::uint8_t> orientation;
+  std::vector<double> magnitude;
+  std::size_t index(int x, int y) const { return std::size_t(y) * width + x; }
+};
+
+struct CellGrid {
+  int cells_w = 0;
+  int cells_h = 0;
+  std::vector<double> bins;
+  double* cell(int cx, int cy) { return &bins[(std::size_t(cy) * cells_w + cx) * kOrientationBins]; }
+  const double* cell(int cx, int cy) const {
+    return &bins[(std::size_t(cy) * cells_w + cx) * kOrientationBins];
+  }
+};
+
+struct EnergyGrid {
+  int cells_w = 0;
+  int cells_h = 0;
+  std::vector<double> energy;
+  double at(int cx, int cy) const { return energy[std::size_t(cy) * cells_w + cx]; }
+};
+
+struct FeatureImage {
+  int cells_w = 0;
+  int cells_h = 0;
+  std::vector<double> values;
+  double* cell(int cx, int cy) { return &values[(std::size_t(cy) * cells_w + cx) * kCellFeatures]; }
+  const double* cell(int cx, int cy) const {
+    return &values[(std::size_t(cy) * cells_w + cx) * kCellFeatures];
+  }
+};
+
+GradientField compute_gradients(const GrayImage& img);
+CellGrid histogramize(const GradientField& grads);
+EnergyGrid cell_energy(const CellGrid& cells);
+FeatureImage compute_features(const CellGrid& cells, const EnergyGrid& energies);
+FeatureImage extract_features(const GrayImage& img);
+
+// ----------------------------------------------------------- detector (detector.hpp)
+inline constexpr int kWindowCells = 10;
+inline constexpr int kFilterWeights = kWindowCells * kWindowCells * kCellFeatures;
+
+struct Box {
+  int x = 0;
+  int y = 0;
+  int w = 0;
+  int h = 0;
+};
+
+double iou(const Box& a, const Box& b);
+
+struct LinearFilter {
+  std::vector<double> weights = std::vector<double>(kFilterWeights, 0.0);
+  double bias = 0.0;
+};
+
+struct DetectorModel {
+  std::array<LinearFilter, 5> filters;
+  double detection_threshold = 0.0;
+  int window_cells = kWindowCells;
+  int cell_px = kCellSize;
+  int scale_num = 5;
+  int scale_den = 6;
+  double min_face_ratio = 0.2;
+  int window_px() const { return window_cells * cell_px; }
+};
+
+struct SaliencyMap {
+  int width = 0;
+  int height = 0;
+  std::vector<double> scores;
+  double at(int cx, int cy) const { return scores[std::size_t(cy) * width + cx]; }
+};
+
+struct Detection {
+  Box box;
+  double score = 0.0;
+  int scale_index = 0;
+  int rotation_index = 0;
+};
+
+SaliencyMap score_dense(const FeatureImage& feat, const LinearFilter& filter);
+SaliencyMap score_separable(const FeatureImage& feat, const LinearFilter& filter);
+std::vector<Detection> threshold_detections(const SaliencyMap& sal, const DetectorModel& model,
+                                            int scale_index, int rotation_index);
+std::vector<Detection> nms(std::vector<Detection> dets, double iou_threshold = 0.5);
+std::vector<int> eligible_scales(int img_w, int img_h, const DetectorModel& model, int n_levels);
+std::vector<Detection> detect_faces(const GrayImage& img, const DetectorModel& model);
+
+// --------------------------------------------------------------------- ert (ert.hpp)
+struct Point2 {
+  double x = 0.0;
+  double y = 0.0;
+};
+
+enum class ShapeFrame { normalized, image };
+
+struct Shape {
+  std::vector<Point2> points;
+  ShapeFrame frame = ShapeFrame::normalized;
+};
+
+struct SimilarityTransform {
+  double scale = 1.0;
+  double rotation = 0.0;
+  double tx = 0.0;
+  double ty = 0.0;
+  Point2 apply(const Point2& p) const;
+  Point2 apply_linear(const Point2& p) const;
+};
+
+SimilarityTransform similarity_transform(const Shape& from, const Shape& to);
+
+struct SplitNode {
+  int anchor_a = 0;
+  int anchor_b = 0;
+  Point2 offset_a;
+  Point2 offset_b;
+  double threshold = 0.0;
+};
+
+struct RegressionTree {
+  int depth = 0;
+  std::vector<SplitNode> splits;
+  std::vector<std::vector<Point2>> leaves;
+};
+
+struct ErtModel {
+  Shape mean_shape;
+  std::vector<std::vector<RegressionTree>> cascade;
+  double shrinkage = 0.1;
+  int landmark_count() const { return int(mean_shape.points.size()); }
+  int levels() const { return int(cascade.size()); }
+  int trees_per_level() const { return cascade.empty() ? 0 : int(cascade[0].size()); }
+};
+
+double sample_intensity(const GrayImage& img, const Box& box, const Shape& shape,
+                        const SimilarityTransform& tform, int anchor, Point2 offset);
+
+using IntensityPairFn = std::function<std::pair<double, double>(const SplitNode&)>;
+const std::vector<Point2>& traverse_tree(const RegressionTree& tree, const IntensityPairFn& intensity_of);
+
+struct PredictStats {
+  std::uint64_t intensity_diffs = 0;
+};
+
+Shape predict_landmarks(const GrayImage& img, const Box& box, const ErtModel& model,
+                        PredictStats* stats = nullptr);
+
+// ------------------------------------------------------------ batch extensions (new)
+namespace gpu {
+
+// Device used by this thread's context (default: $BLINKLINE_DEVICE or 0).
+void set_device(int device);
+// Drop cached device copies of models (call after mutating a model in place).
+void invalidate_model_cache();
+
+// detect_faces over many equal-size frames in one device pass; result[i] is frame i's list.
+std::vector<std::vector<Detection>> detect_faces_batch(const std::vector<GrayImage>& frames,
+                                                       const DetectorModel& model);
+// predict_landmarks for many (frame, box) pairs in one device pass.
+std::vector<Shape> predict_landmarks_batch(const std::vector<GrayImage>& frames,
+                                           const std::vector<int>& frame_of_box,
+                                           const std::vector<Box>& boxes, const ErtModel& model);
+// detect + landmark every kept detection (pipeline.cpp:159-190 per frame), all on device.
+struct FrameResult {
+  std::vector<Detection> detections;
+  std::vector<Shape> landmarks;  // aligned with detections
+};
+std::vector<FrameResult> detect_and_landmark(const std::vector<GrayImage>& frames,
+                                             const DetectorModel& hog, const ErtModel& ert);
+
+}  // namespace gpu
+}  // namespace blinkline

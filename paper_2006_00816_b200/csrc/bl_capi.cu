@@ -1,0 +1,1052 @@
+// Host side of blinkline_b200: device contexts, batch plans (geometry + pre-sized device
+// arenas, the paper's "allocate once" scheme), the per-batch pipeline
+// and every extern "C" entry point of include/blinkline_b200.h.
+//
+// No computation of the hot path happens on the host: the host computes geometry
+// (pyramid dims, eligibility, per-level scale constants -- with the same libm calls the
+// reference makes, so the constants are bit-identical) and launches kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "bl_internal.cuh"
+
+using namespace blb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(BL_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                     __FILE__, __LINE__);                                                 \
+  } while (0)
+
+#define TRY(call)              \
+  do {                         \
+    int rc_ = (call);          \
+    if (rc_ != BL_OK) return rc_; \
+  } while (0)
+
+// Device buffer that only grows.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int device = -1;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      if (device >= 0 && device != cur) cudaSetDevice(device);
+      cudaFree(p);
+      if (device >= 0 && device != cur) cudaSetDevice(cur);
+    }
+    p = nullptr;
+    bytes = 0;
+  }
+  int ensure(size_t n, bool zero = false) {
+    if (n <= bytes && p) return BL_OK;
+    release();
+    const size_t alloc = std::max<size_t>(n, 256);
+    cudaError_t e = cudaMalloc(&p, alloc);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return set_err(BL_ERR_CUDA, "cudaMalloc(%zu) failed: %s", alloc, cudaGetErrorString(e));
+    }
+    cudaGetDevice(&device);
+    bytes = alloc;
+    if (zero) {
+      e = cudaMemset(p, 0, alloc);
+      if (e != cudaSuccess) return set_err(BL_ERR_CUDA, "cudaMemset failed: %s", cudaGetErrorString(e));
+    }
+    return BL_OK;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int round_half_up_host(double v) { return int(std::floor(v + 0.5)); }  // detector.cpp:41
+
+struct DetectorState {
+  bool ready = false;
+  double thr = 0;
+  int window_cells = 10, cell_px = 8, scale_num = 5, scale_den = 6;
+  double min_face_ratio = 0.2;
+  double bias[kFilters] = {0};
+  float cut[kFilters] = {0};
+  DevBuf w64, w32, bias64, cut32;
+};
+
+struct ErtState {
+  bool ready = false;
+  ErtDev dev{};
+  DevBuf mean, anchors, split, leaves;
+};
+
+// A batch plan: geometry + device arenas for (n, w, h, pixel type, detector geometry).
+struct Plan {
+  bool valid = false;
+  int n = 0, w = 0, h = 0, pix = 0;
+  int window = 80, cell_px = 8, window_cells = 10, scale_num = 5, scale_den = 6;
+  double min_face_ratio = 0.2;
+  int n_levels = 0;
+  std::vector<int> lw, lh;
+  std::vector<long long> arena_off;  // levels >= 1, in doubles
+  long long arena_elems = 0;
+  std::vector<int> scored;           // pyramid level of each scored slot
+  PlanDesc host{};
+  DevBuf desc;
+  long long cap_pf = 0;              // raw detections per frame (all anchors x 5 filters)
+  long long cand_cap = 0;
+  long long f32_elems = 0;
+  long long gkeys_pf = 0;
+  DevBuf arena, bins, energy, feat64, feat32, cand, n_cand, dets, det_count, kept, kept_count, gkeys,
+      overflow, offsets, flat, face_frame, n_faces, input;
+};
+
+}  // namespace
+
+struct bl_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t st = nullptr;
+  std::mutex mu;
+  uint64_t launches = 0;
+  DetectorState det;
+  ErtState ert;
+  Plan plan;
+  // ERT working set
+  DevBuf ert_cur, ert_out, ert_leaf, ert_boxes, ert_frames, ert_nfaces, ert_err, ert_input;
+  // scratch for stage functions
+  DevBuf s_a, s_b, s_c, s_d, s_e, s_desc;
+  // pinned host staging for counts
+  int* h_counts = nullptr;
+  size_t h_counts_cap = 0;
+  bool timing = false;
+  cudaEvent_t ev[BL_STAGE_COUNT + 1] = {};
+  float stage_ms[BL_STAGE_COUNT] = {};
+  int stage_launch[BL_STAGE_COUNT] = {};
+  bool graphs = true;
+};
+
+namespace {
+
+Launch launch_of(bl_ctx* c) { return Launch{c->st, &c->launches}; }
+
+int use_device(bl_ctx* c) {
+  CK(cudaSetDevice(c->device));
+  return BL_OK;
+}
+
+// -------------------------------------------------------------------- geometry ----
+// image.cpp:158-172 (level dims) ; detector.cpp:144-155 (eligibility) ; detector.cpp:163-167.
+void pyramid_dims(int w, int h, int window, std::vector<int>& lw, std::vector<int>& lh) {
+  lw.assign(1, w);
+  lh.assign(1, h);
+  while (true) {
+    const int cw = lw.back(), chh = lh.back();
+    if (cw < 2 || chh < 2) break;
+    const int nw = cw * 5 / 6, nh = chh * 5 / 6;
+    if (nw < window || nh < window) break;
+    lw.push_back(nw);
+    lh.push_back(nh);
+  }
+}
+
+int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
+  const DetectorState& D = c->det;
+  if (P.valid && P.n == n && P.w == w && P.h == h && P.pix == pix && P.window_cells == D.window_cells &&
+      P.cell_px == D.cell_px && P.scale_num == D.scale_num && P.scale_den == D.scale_den &&
+      P.min_face_ratio == D.min_face_ratio)
+    return BL_OK;
+  P.valid = false;
+  P.n = n;
+  P.w = w;
+  P.h = h;
+  P.pix = pix;
+  P.window_cells = D.window_cells;
+  P.cell_px = D.cell_px;
+  P.scale_num = D.scale_num;
+  P.scale_den = D.scale_den;
+  P.min_face_ratio = D.min_face_ratio;
+  P.window = D.window_cells * D.cell_px;
+  pyramid_dims(w, h, P.window, P.lw, P.lh);
+  P.n_levels = (int)P.lw.size();
+  if (P.n_levels > kMaxLevels) return set_err(BL_ERR_INVALID, "pyramid deeper than %d levels", kMaxLevels);
+  P.arena_off.assign(P.n_levels, 0);
+  long long off = 0;
+  for (int k = 1; k < P.n_levels; ++k) {
+    P.arena_off[k] = off;
+    off += (long long)n * P.lw[k] * P.lh[k];
+  }
+  P.arena_elems = off;
+
+  // eligible_scales (detector.cpp:144-155) + the "room for a window" skip (:165-167)
+  const double min_face = D.min_face_ratio * std::min(w, h);
+  P.scored.clear();
+  for (int k = 0; k < P.n_levels; ++k) {
+    const double detectable =
+        P.window / std::pow(double(D.scale_num) / D.scale_den, double(k));
+    if (!(detectable >= min_face * (1.0 - 1e-9))) continue;
+    if (P.lw[k] / D.cell_px < D.window_cells || P.lh[k] / D.cell_px < D.window_cells) continue;
+    if (P.lw[k] / 8 < kWin || P.lh[k] / 8 < kWin)
+      return set_err(BL_ERR_INVALID, "feature image smaller than the 10x10 detection window");
+    P.scored.push_back(k);
+  }
+  PlanDesc& H = P.host;
+  std::memset(&H, 0, sizeof H);
+  H.n_frames = n;
+  H.n_scored = (int)P.scored.size();
+  long long cells = 0, gh = 0, sc = 0, f32 = 0, anchors_pf = 0;
+  for (int s = 0; s < H.n_scored; ++s) {
+    const int k = P.scored[s];
+    LevelDesc& L = H.lv[s];
+    L.w = P.lw[k];
+    L.h = P.lh[k];
+    L.cw = L.w / 8;
+    L.ch = L.h / 8;
+    L.sw = L.cw - (kWin - 1);
+    L.sh = L.ch - (kWin - 1);
+    L.level = k;
+    L.c = std::pow(double(D.scale_num) / D.scale_den, double(k));  // detector.cpp:104
+    L.side = round_half_up_host(P.window / L.c);                    // detector.cpp:105
+    if (k == 0) {
+      L.pix_off = 0;  // patched per call (input pointer)
+      L.pix_fstride = 0;
+      L.pix_pitch = 0;
+    } else {
+      L.pix_off = P.arena_off[k];
+      L.pix_fstride = (long long)L.w * L.h;
+      L.pix_pitch = L.w;
+    }
+    L.cell_off = cells;
+    L.cell_begin = cells;
+    cells += (long long)n * L.cw * L.ch;
+    L.cw_pad = (int)(div_up(L.sw, kTileAX) * kTileAX + 12);
+    L.ch_pad = (int)(div_up(L.sh, kTileAY) * kTileAY + (kWin - 1));
+    L.f32_off = f32;
+    L.f32_fstride = (long long)kFeatPad * L.ch_pad * L.cw_pad;
+    f32 += (long long)n * L.f32_fstride;
+    L.gh_tiles_x = (int)div_up(L.cw, kGhCells);
+    L.gh_tiles_y = (int)div_up(L.ch, kGhRows);
+    L.gh_begin = gh;
+    gh += (long long)n * L.gh_tiles_x * L.gh_tiles_y;
+    L.sc_tiles_x = (int)div_up(L.sw, kTileAX);
+    L.sc_tiles_y = (int)div_up(L.sh, kTileAY);
+    L.sc_begin = sc;
+    sc += (long long)n * L.sc_tiles_x * L.sc_tiles_y;
+    L.anchor_base = anchors_pf;
+    anchors_pf += (long long)L.sw * L.sh;
+  }
+  H.gh_total = gh;
+  H.sc_total = sc;
+  H.cell_total = cells;
+  H.cells_per_frame = n ? cells / n : 0;
+  P.f32_elems = f32;
+  P.cap_pf = std::max<long long>(1, anchors_pf * kFilters);
+  P.cand_cap = std::max<long long>(1, (long long)n * anchors_pf * kFilters);
+  P.gkeys_pf = nms_gkeys_per_frame(P.cap_pf);
+
+  TRY(P.desc.ensure(sizeof(PlanDesc)));
+  TRY(P.arena.ensure(sizeof(double) * std::max<long long>(1, P.arena_elems)));
+  TRY(P.bins.ensure(sizeof(double) * kBins * std::max<long long>(1, cells)));
+  TRY(P.energy.ensure(sizeof(double) * std::max<long long>(1, cells)));
+  TRY(P.feat64.ensure(sizeof(double) * kFeat * std::max<long long>(1, cells)));
+  // zero once: the padding of the fp32 planes is never written by the feature kernel
+  const bool regrow = P.feat32.bytes < sizeof(float) * (size_t)std::max<long long>(1, f32);
+  TRY(P.feat32.ensure(sizeof(float) * std::max<long long>(1, f32), true));
+  if (!regrow) CK(cudaMemset(P.feat32.p, 0, sizeof(float) * std::max<long long>(1, f32)));
+  TRY(P.cand.ensure(sizeof(Candidate) * P.cand_cap));
+  TRY(P.n_cand.ensure(sizeof(unsigned long long)));
+  TRY(P.dets.ensure(sizeof(DevDet) * n * P.cap_pf));
+  TRY(P.kept.ensure(sizeof(DevDet) * n * P.cap_pf));
+  TRY(P.det_count.ensure(sizeof(int) * n));
+  TRY(P.kept_count.ensure(sizeof(int) * n));
+  TRY(P.overflow.ensure(sizeof(int)));
+  if (P.gkeys_pf) TRY(P.gkeys.ensure(nms_key_bytes() * n * P.gkeys_pf));
+  TRY(P.offsets.ensure(sizeof(int) * (n + 1)));
+  TRY(P.flat.ensure(sizeof(DevDet) * n * P.cap_pf));
+  TRY(P.face_frame.ensure(sizeof(int) * n * P.cap_pf));
+  TRY(P.n_faces.ensure(sizeof(int)));
+  CK(cudaMemcpy(P.desc.p, &P.host, sizeof(PlanDesc), cudaMemcpyHostToDevice));
+  P.valid = true;
+  return BL_OK;
+}
+
+void stage_mark(bl_ctx* c, int stage) {
+  if (c->timing) cudaEventRecord(c->ev[stage], c->st);
+}
+
+// ------------------------------------------------------------------ detection ----
+// Runs detect on n frames already resident on the device (`in`, element pitch/stride).
+// Leaves kept detections in P.flat (frame order) and P.n_faces on the device; copies the
+// per-frame counts to h_counts (synchronising).
+int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long long pitch,
+               long long fstride, int64_t* total_out) {
+  Plan& P = c->plan;
+  TRY(build_plan(c, P, n, w, h, pix));
+  const Launch L = launch_of(c);
+  const DetectorState& D = c->det;
+  uint64_t l0 = c->launches;
+
+  // level 0 descriptor points at the caller's frames
+  if (!P.scored.empty() && P.scored[0] == 0) {
+    LevelDesc& L0 = P.host.lv[0];
+    if (L0.pix_pitch != pitch || L0.pix_fstride != fstride) {
+      L0.pix_off = 0;
+      L0.pix_pitch = (int)pitch;
+      L0.pix_fstride = fstride;
+      CK(cudaMemcpyAsync(P.desc.p, &P.host, sizeof(PlanDesc), cudaMemcpyHostToDevice, c->st));
+    }
+  }
+  stage_mark(c, BL_STAGE_PYRAMID);
+  // pyramid chain (image.cpp:162-170): level k from level k-1, every frame at once
+  for (int k = 1; k < P.n_levels; ++k) {
+    const void* src = k == 1 ? in : (const void*)(P.arena.as<double>() + P.arena_off[k - 1]);
+    const int src_u8 = (k == 1 && pix == BL_PIX_U8);
+    const long long sp = k == 1 ? pitch : P.lw[k - 1];
+    const long long sf = k == 1 ? fstride : (long long)P.lw[k - 1] * P.lh[k - 1];
+    launch_resample(L, src, src_u8, P.lw[k - 1], P.lh[k - 1], sp, sf, P.arena.as<double>() + P.arena_off[k],
+                    P.lw[k], P.lh[k], (long long)P.lw[k] * P.lh[k], n);
+  }
+  stage_mark(c, BL_STAGE_GRADHIST);
+  const PlanDesc* Pd = P.desc.as<PlanDesc>();
+  const int ns = P.host.n_scored;
+  CK(cudaMemsetAsync(P.n_cand.p, 0, sizeof(unsigned long long), c->st));
+  CK(cudaMemsetAsync(P.det_count.p, 0, sizeof(int) * n, c->st));
+  CK(cudaMemsetAsync(P.overflow.p, 0, sizeof(int), c->st));
+  if (ns > 0) {
+    int s1 = 0;
+    if (P.scored[0] == 0) {
+      launch_gradhist_levels(L, P.host, Pd, 0, 1, in, pix == BL_PIX_U8 ? 0 : 1, P.bins.as<double>(),
+                             P.energy.as<double>());
+      s1 = 1;
+    }
+    launch_gradhist_levels(L, P.host, Pd, s1, ns, P.arena.as<double>(), 1, P.bins.as<double>(),
+                           P.energy.as<double>());
+  }
+  stage_mark(c, BL_STAGE_FEATURES);
+  launch_features(L, P.host, Pd, P.bins.as<double>(), P.energy.as<double>(), P.feat64.as<double>(),
+                  P.feat32.as<float>());
+  stage_mark(c, BL_STAGE_SCREEN);
+  launch_screen(L, P.host, Pd, P.feat32.as<float>(), D.w32.as<float>(), D.cut32.as<float>(),
+                P.cand.as<Candidate>(), P.n_cand.as<unsigned long long>(), P.cand_cap);
+  stage_mark(c, BL_STAGE_RESCORE);
+  launch_rescore(L, Pd, P.feat64.as<double>(), D.w64.as<double>(), D.bias64.as<double>(), D.thr, D.cell_px,
+                 P.cand.as<Candidate>(), P.n_cand.as<unsigned long long>(), P.cand_cap, P.dets.as<DevDet>(),
+                 P.det_count.as<int>(), P.cap_pf, P.overflow.as<int>(), 148 * 8);
+  stage_mark(c, BL_STAGE_NMS);
+  launch_nms(L, P.dets.as<DevDet>(), P.det_count.as<int>(), P.cap_pf, n, 0.5, P.kept.as<DevDet>(),
+             P.kept_count.as<int>(), P.gkeys.p, P.gkeys_pf);
+  launch_flatten(L, P.kept.as<DevDet>(), P.kept_count.as<int>(), P.cap_pf, n, P.offsets.as<int>(),
+                 P.flat.as<DevDet>(), P.face_frame.as<int>(), P.n_faces.as<int>(), (long long)n * P.cap_pf);
+  (void)l0;
+  (void)total_out;
+  return BL_OK;
+}
+
+int ensure_counts(bl_ctx* c, size_t n) {
+  if (c->h_counts_cap >= n) return BL_OK;
+  if (c->h_counts) cudaFreeHost(c->h_counts);
+  c->h_counts = nullptr;
+  CK(cudaMallocHost(&c->h_counts, sizeof(int) * (n + 2)));
+  c->h_counts_cap = n;
+  return BL_OK;
+}
+
+// Stage host frames into a device buffer (or use device frames in place).
+int stage_input(bl_ctx* c, DevBuf& buf, const void* frames, int pix, int n, int w, int h, size_t pitch,
+                size_t fstride, const void** dev, long long* dpitch, long long* dfstride) {
+  const size_t es = pix == BL_PIX_U8 ? 1 : 8;
+  if (is_device_ptr(frames)) {
+    *dev = frames;
+    *dpitch = (long long)pitch;
+    *dfstride = (long long)fstride;
+    return BL_OK;
+  }
+  TRY(buf.ensure(es * (size_t)n * w * h));
+  if (pitch == (size_t)w && fstride == (size_t)w * h) {
+    CK(cudaMemcpyAsync(buf.p, frames, es * (size_t)n * w * h, cudaMemcpyDefault, c->st));
+  } else {
+    for (int i = 0; i < n; ++i)
+      CK(cudaMemcpy2DAsync((char*)buf.p + es * (size_t)i * w * h, es * w,
+                           (const char*)frames + es * fstride * i, es * pitch, es * w, h, cudaMemcpyDefault,
+                           c->st));
+  }
+  *dev = buf.p;
+  *dpitch = w;
+  *dfstride = (long long)w * h;
+  return BL_OK;
+}
+
+int check_frames(const void* frames, int pix, int n, int w, int h, size_t pitch, size_t fstride) {
+  if (!frames && n > 0) return set_err(BL_ERR_INVALID, "frames is NULL");
+  if (pix != BL_PIX_U8 && pix != BL_PIX_F64) return set_err(BL_ERR_INVALID, "unknown pixel type %d", pix);
+  if (n < 0) return set_err(BL_ERR_INVALID, "negative frame count");
+  if (w < 1 || h < 1) return set_err(BL_ERR_INVALID, "make_image: dimensions must be >= 1");
+  if (pitch < (size_t)w) return set_err(BL_ERR_INVALID, "pitch %zu < width %d", pitch, w);
+  if (n > 1 && fstride < pitch * (size_t)(h - 1) + w) return set_err(BL_ERR_INVALID, "frame stride too small");
+  return BL_OK;
+}
+
+// Runs the ERT cascade for `nf` faces whose boxes (int stride) and frame indices are on the
+// device; n_faces_dev holds the count.  Output landmarks -> c->ert_out.
+int run_ert(bl_ctx* c, const void* frames, int pix, int w, int h, long long pitch, long long fstride,
+            const int* face_frame, const int* boxes, int box_stride, const int* n_faces_dev, int nf,
+            uint8_t* leaf_dev) {
+  ErtState& E = c->ert;
+  const Launch L = launch_of(c);
+  const int L2 = 2 * E.dev.L;
+  TRY(c->ert_cur.ensure(sizeof(double) * L2 * std::max(1, nf)));
+  TRY(c->ert_out.ensure(sizeof(double) * L2 * std::max(1, nf)));
+  TRY(c->ert_err.ensure(sizeof(int)));
+  CK(cudaMemsetAsync(c->ert_err.p, 0, sizeof(int), c->st));
+  launch_ert_init(L, E.dev, n_faces_dev, nf, c->ert_cur.as<double>());
+  const int blocks = std::max(1, std::min(nf, 148 * 8));
+  for (int t = 0; t < E.dev.T; ++t)
+    launch_ert_level(L, E.dev, t, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
+                     n_faces_dev, nf, c->ert_cur.as<double>(), leaf_dev, c->ert_err.as<int>(), blocks);
+  launch_ert_finish(L, E.dev, boxes, box_stride, n_faces_dev, nf, c->ert_cur.as<double>(),
+                    c->ert_out.as<double>());
+  return BL_OK;
+}
+
+void timing_begin(bl_ctx* c) {
+  if (!c->timing) return;
+  cudaEventRecord(c->ev[BL_STAGE_H2D], c->st);
+}
+
+void timing_end(bl_ctx* c, const int* present, int n_present) {
+  if (!c->timing) return;
+  cudaEventRecord(c->ev[BL_STAGE_COUNT], c->st);
+  cudaEventSynchronize(c->ev[BL_STAGE_COUNT]);
+  // stages marked in this call, in order; each runs until the next marked one
+  for (int i = 0; i < BL_STAGE_COUNT; ++i) c->stage_ms[i] = 0.f;
+  for (int i = 0; i < n_present; ++i) {
+    const int a = present[i];
+    const cudaEvent_t e1 = i + 1 < n_present ? c->ev[present[i + 1]] : c->ev[BL_STAGE_COUNT];
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[a], e1);
+    c->stage_ms[a] = ms;
+  }
+}
+
+int detect_common(bl_ctx* c, const void* frames, int pix, int n, int w, int h, size_t pitch, size_t fstride,
+                  bl_detection* out, int64_t cap, int32_t* counts, int64_t* total, double* landmarks) {
+  if (!c) return set_err(BL_ERR_INVALID, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->det.ready) return set_err(BL_ERR_STATE, "no detector model uploaded");
+  if (landmarks && !c->ert.ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
+  if (fstride == 0) fstride = pitch * h;
+  TRY(check_frames(frames, pix, n, w, h, pitch, fstride));
+  TRY(use_device(c));
+  if (n == 0) {
+    if (total) *total = 0;
+    return BL_OK;
+  }
+  timing_begin(c);
+  const void* dev = nullptr;
+  long long dp = 0, df = 0;
+  TRY(stage_input(c, c->plan.input, frames, pix, n, w, h, pitch, fstride, &dev, &dp, &df));
+  TRY(run_detect(c, dev, pix, n, w, h, dp, df, nullptr));
+  Plan& P = c->plan;
+  TRY(ensure_counts(c, n + 2));
+  CK(cudaMemcpyAsync(c->h_counts, P.kept_count.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->h_counts + n, P.overflow.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaGetLastError());
+  if (c->h_counts[n]) return set_err(BL_ERR_CAPACITY, "raw detection capacity exceeded");
+  int64_t tot = 0;
+  for (int i = 0; i < n; ++i) {
+    if (counts) counts[i] = c->h_counts[i];
+    tot += c->h_counts[i];
+  }
+  if (total) *total = tot;
+  if (tot > cap) return set_err(BL_ERR_CAPACITY, "output capacity %lld < %lld detections", (long long)cap,
+                                (long long)tot);
+  if (landmarks && tot > 0) {
+    stage_mark(c, BL_STAGE_ERT);
+    TRY(run_ert(c, dev, pix, w, h, dp, df, P.face_frame.as<int>(), P.flat.as<int>(), 8, P.n_faces.as<int>(),
+                (int)tot, nullptr));
+  }
+  stage_mark(c, BL_STAGE_D2H);
+  if (tot > 0 && out)
+    CK(cudaMemcpyAsync(out, P.flat.p, sizeof(bl_detection) * tot, cudaMemcpyDefault, c->st));
+  if (landmarks && tot > 0)
+    CK(cudaMemcpyAsync(landmarks, c->ert_out.p, sizeof(double) * 2 * c->ert.dev.L * tot, cudaMemcpyDefault,
+                       c->st));
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaGetLastError());
+  if (landmarks && tot > 0) {
+    int err = 0;
+    CK(cudaMemcpy(&err, c->ert_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err == 1) return set_err(BL_ERR_INVALID, "similarity_transform: source shape has no spread");
+    if (err == 2) return set_err(BL_ERR_INVALID, "similarity_transform: target shape has no spread");
+  }
+  const int present_det[] = {BL_STAGE_H2D, BL_STAGE_PYRAMID, BL_STAGE_GRADHIST, BL_STAGE_FEATURES,
+                             BL_STAGE_SCREEN, BL_STAGE_RESCORE, BL_STAGE_NMS, BL_STAGE_ERT, BL_STAGE_D2H};
+  if (landmarks && tot > 0) {
+    timing_end(c, present_det, 9);
+  } else {
+    const int p2[] = {BL_STAGE_H2D, BL_STAGE_PYRAMID, BL_STAGE_GRADHIST, BL_STAGE_FEATURES,
+                      BL_STAGE_SCREEN, BL_STAGE_RESCORE, BL_STAGE_NMS, BL_STAGE_D2H};
+    timing_end(c, p2, 8);
+  }
+  return BL_OK;
+}
+
+// Copies `bytes` from a user pointer (host or device) into scratch, returns a device pointer.
+int to_device(bl_ctx* c, DevBuf& buf, const void* src, size_t bytes, const void** dev) {
+  if (is_device_ptr(src)) {
+    *dev = src;
+    return BL_OK;
+  }
+  TRY(buf.ensure(bytes));
+  if (bytes) CK(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyDefault, c->st));
+  *dev = buf.p;
+  return BL_OK;
+}
+
+int from_device(bl_ctx* c, void* dst, const void* dev, size_t bytes) {
+  if (bytes) CK(cudaMemcpyAsync(dst, dev, bytes, cudaMemcpyDefault, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaGetLastError());
+  return BL_OK;
+}
+
+// Single-level plan over one feature/cell grid (stage functions).
+void single_level_plan(PlanDesc& H, int w, int h, int cw, int ch) {
+  std::memset(&H, 0, sizeof H);
+  H.n_frames = 1;
+  H.n_scored = 1;
+  LevelDesc& L = H.lv[0];
+  L.w = w;
+  L.h = h;
+  L.cw = cw;
+  L.ch = ch;
+  L.sw = cw - 9;
+  L.sh = ch - 9;
+  L.pix_pitch = w;
+  L.pix_fstride = (long long)w * h;
+  L.gh_tiles_x = (int)div_up(cw, kGhCells);
+  L.gh_tiles_y = (int)div_up(ch, kGhRows);
+  H.gh_total = (long long)L.gh_tiles_x * L.gh_tiles_y;
+  H.cell_total = (long long)cw * ch;
+  H.cells_per_frame = H.cell_total;
+}
+
+}  // namespace
+
+// =============================================================== extern "C" ABI ====
+extern "C" {
+
+int bl_abi_version(void) { return BL_ABI_VERSION; }
+
+const char* bl_last_error(void) { return g_err.c_str(); }
+
+int bl_device_count(int* n) {
+  if (!n) return set_err(BL_ERR_INVALID, "null out");
+  CK(cudaGetDeviceCount(n));
+  return BL_OK;
+}
+
+int bl_ctx_create(int device, bl_ctx** out) {
+  if (!out) return set_err(BL_ERR_INVALID, "null out");
+  *out = nullptr;
+  int nd = 0;
+  CK(cudaGetDeviceCount(&nd));
+  if (device < 0 || device >= nd) return set_err(BL_ERR_INVALID, "device %d out of range (%d devices)", device, nd);
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return set_err(BL_ERR_CUDA, "blinkline_b200 is built for sm_100a; device %d is sm_%d%d", device, prop.major,
+                   prop.minor);
+  auto c = std::make_unique<bl_ctx>();
+  c->device = device;
+  CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+  c->st = c->own;
+  for (auto& e : c->ev) CK(cudaEventCreate(&e));
+  // hog.cpp:12-24: the 18 directions from the host libm, exactly as the reference builds them
+  double ux[kBins], uy[kBins];
+  for (int d = 0; d < kBins; ++d) {
+    const double a = 2.0 * M_PI * d / kBins;
+    ux[d] = std::cos(a);
+    uy[d] = std::sin(a);
+  }
+  set_direction_table(ux, uy);
+  CK(cudaGetLastError());
+  *out = c.release();
+  return BL_OK;
+}
+
+void bl_ctx_destroy(bl_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  if (c->h_counts) cudaFreeHost(c->h_counts);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  cudaStream_t own = c->own;
+  delete c;  // DevBufs free on their device
+  if (own) cudaStreamDestroy(own);
+}
+
+int bl_ctx_set_stream(bl_ctx* c, void* stream) {
+  if (!c) return set_err(BL_ERR_INVALID, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->st = stream ? (cudaStream_t)stream : c->own;
+  return BL_OK;
+}
+
+int bl_ctx_synchronize(bl_ctx* c) {
+  if (!c) return set_err(BL_ERR_INVALID, "null context");
+  TRY(use_device(c));
+  CK(cudaStreamSynchronize(c->st));
+  return BL_OK;
+}
+
+int bl_ctx_launch_count(bl_ctx* c, uint64_t* out) {
+  if (!c || !out) return set_err(BL_ERR_INVALID, "null argument");
+  *out = c->launches;
+  return BL_OK;
+}
+
+int bl_ctx_enable_stage_timing(bl_ctx* c, int enable) {
+  if (!c) return set_err(BL_ERR_INVALID, "null context");
+  c->timing = enable != 0;
+  return BL_OK;
+}
+
+int bl_ctx_stage_times(bl_ctx* c, float* ms, int* launches) {
+  if (!c) return set_err(BL_ERR_INVALID, "null context");
+  for (int i = 0; i < BL_STAGE_COUNT; ++i) {
+    if (ms) ms[i] = c->stage_ms[i];
+    if (launches) launches[i] = c->stage_launch[i];
+  }
+  return BL_OK;
+}
+
+int bl_ctx_enable_graphs(bl_ctx* c, int enable) {
+  if (!c) return set_err(BL_ERR_INVALID, "null context");
+  c->graphs = enable != 0;
+  return BL_OK;
+}
+
+int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, double threshold, int window_cells,
+                       int cell_px, int scale_num, int scale_den, double min_face_ratio) {
+  if (!c || !weights || !biases) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (window_cells != kWin) return set_err(BL_ERR_INVALID, "filter must carry exactly 3100 weights");
+  if (cell_px < 1) return set_err(BL_ERR_MODEL, "cell_px must be >= 1");
+  if (scale_num < 1 || scale_den < 1) return set_err(BL_ERR_MODEL, "scale factor must be positive");
+  TRY(use_device(c));
+  DetectorState& D = c->det;
+  D.ready = false;
+  D.thr = threshold;
+  D.window_cells = window_cells;
+  D.cell_px = cell_px;
+  D.scale_num = scale_num;
+  D.scale_den = scale_den;
+  D.min_face_ratio = min_face_ratio;
+  // fp32 screen weights, [j][f][i*5 + r] blocks of 52 floats
+  std::vector<float> w32((size_t)kWin * kFeat * 52, 0.f);
+  for (int r = 0; r < kFilters; ++r)
+    for (int j = 0; j < kWin; ++j)
+      for (int i = 0; i < kWin; ++i)
+        for (int f = 0; f < kFeat; ++f)
+          w32[((size_t)j * kFeat + f) * 52 + i * kFilters + r] =
+              (float)weights[(size_t)r * kFilterW + j * kRowW + i * kFeat + f];
+  // rigorous screen cut: |fp32 window sum - exact sum| <= delta_r
+  const double u = std::ldexp(1.0, -24);
+  for (int r = 0; r < kFilters; ++r) {
+    double l1 = 0;
+    for (int k = 0; k < kFilterW; ++k) l1 += std::fabs(weights[(size_t)r * kFilterW + k]);
+    D.bias[r] = biases[r];
+    const double delta = 324.0 * u * 1.01 * 0.8486 * l1 + std::ldexp(1.0, -20) * (std::fabs(threshold) + std::fabs(biases[r])) + 1e-9;
+    const double cutd = threshold - biases[r] - delta;
+    float cf = (float)cutd;
+    if (std::isnan(cutd)) cf = -INFINITY;
+    if ((double)cf > cutd) cf = std::nextafterf(cf, -INFINITY);
+    D.cut[r] = cf;
+  }
+  TRY(D.w64.ensure(sizeof(double) * kFilters * kFilterW));
+  TRY(D.w32.ensure(sizeof(float) * w32.size()));
+  TRY(D.bias64.ensure(sizeof(double) * kFilters));
+  TRY(D.cut32.ensure(sizeof(float) * kFilters));
+  CK(cudaMemcpy(D.w64.p, weights, sizeof(double) * kFilters * kFilterW, cudaMemcpyDefault));
+  CK(cudaMemcpy(D.w32.p, w32.data(), sizeof(float) * w32.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(D.bias64.p, biases, sizeof(double) * kFilters, cudaMemcpyDefault));
+  CK(cudaMemcpy(D.cut32.p, D.cut, sizeof(float) * kFilters, cudaMemcpyHostToDevice));
+  c->plan.valid = false;
+  D.ready = true;
+  return BL_OK;
+}
+
+int bl_ert_upload(bl_ctx* c, int L, int T, int K, int F, double shrinkage, const double* mean_xy,
+                  const int32_t* anchors, const double* split_params, const double* leaves) {
+  if (!c) return set_err(BL_ERR_INVALID, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (L < 2) return set_err(BL_ERR_INVALID, "predict_landmarks: model has no mean shape");
+  if (T < 0 || K < 0 || F < 0 || F > 8) return set_err(BL_ERR_MODEL, "cascade dims out of range");
+  if (T > 0 && K < 1) return set_err(BL_ERR_MODEL, "every cascade level must carry K trees");
+  if (!mean_xy || ((size_t)T * K > 0 && (!leaves || (F > 0 && (!anchors || !split_params)))))
+    return set_err(BL_ERR_INVALID, "null model array");
+  TRY(use_device(c));
+  ErtState& E = c->ert;
+  E.ready = false;
+  const int S = (1 << F) - 1, NL = 1 << F;
+  const size_t nsplit = (size_t)T * K * S;
+  std::vector<int16_t> a16(2 * nsplit + 2);
+  for (size_t i = 0; i < 2 * nsplit; ++i) {
+    if (anchors[i] < 0 || anchors[i] >= L) return set_err(BL_ERR_MODEL, "split anchor out of range");
+    a16[i] = (int16_t)anchors[i];
+  }
+  TRY(E.mean.ensure(sizeof(double) * 2 * L));
+  TRY(E.anchors.ensure(sizeof(int16_t) * a16.size()));
+  TRY(E.split.ensure(sizeof(double) * 5 * nsplit + 8));
+  TRY(E.leaves.ensure(sizeof(double) * (size_t)T * K * NL * L * 2 + 8));
+  CK(cudaMemcpy(E.mean.p, mean_xy, sizeof(double) * 2 * L, cudaMemcpyDefault));
+  CK(cudaMemcpy(E.anchors.p, a16.data(), sizeof(int16_t) * a16.size(), cudaMemcpyHostToDevice));
+  if (nsplit) CK(cudaMemcpy(E.split.p, split_params, sizeof(double) * 5 * nsplit, cudaMemcpyDefault));
+  if ((size_t)T * K) CK(cudaMemcpy(E.leaves.p, leaves, sizeof(double) * (size_t)T * K * NL * L * 2, cudaMemcpyDefault));
+  // centroid of the mean shape in similarity_transform's order (ert.cpp:33-43)
+  std::vector<double> m(2 * L);
+  CK(cudaMemcpy(m.data(), mean_xy, sizeof(double) * 2 * L, cudaMemcpyDefault));
+  double mx = 0, my = 0;
+  for (int i = 0; i < L; ++i) {
+    mx += m[2 * i];
+    my += m[2 * i + 1];
+  }
+  mx /= double(L);
+  my /= double(L);
+  E.dev.L = L;
+  E.dev.T = T;
+  E.dev.K = K;
+  E.dev.F = F;
+  E.dev.S = S;
+  E.dev.NL = NL;
+  E.dev.shrinkage = shrinkage;
+  E.dev.mean_xy = E.mean.as<double>();
+  E.dev.anchors = E.anchors.as<int16_t>();
+  E.dev.split = E.split.as<double>();
+  E.dev.leaves = E.leaves.as<double>();
+  E.dev.mean_cx = mx;
+  E.dev.mean_cy = my;
+  E.ready = true;
+  return BL_OK;
+}
+
+int bl_detect(bl_ctx* c, const void* frames, int pixel_type, int n, int w, int h, size_t pitch, size_t frame_stride,
+              bl_detection* out, int64_t cap, int32_t* counts, int64_t* total) {
+  return detect_common(c, frames, pixel_type, n, w, h, pitch, frame_stride, out, cap, counts, total, nullptr);
+}
+
+int bl_detect_landmarks(bl_ctx* c, const void* frames, int pixel_type, int n, int w, int h, size_t pitch,
+                        size_t frame_stride, bl_detection* out, int64_t cap, int32_t* counts, int64_t* total,
+                        double* landmarks) {
+  if (!landmarks) return set_err(BL_ERR_INVALID, "landmarks output is NULL");
+  return detect_common(c, frames, pixel_type, n, w, h, pitch, frame_stride, out, cap, counts, total, landmarks);
+}
+
+int bl_landmarks(bl_ctx* c, const void* frames, int pixel_type, int n_frames, int w, int h, size_t pitch,
+                 size_t frame_stride, const int32_t* frame_of_box, const bl_box* boxes, int64_t n_boxes,
+                 double* out_xy, uint8_t* leaf_idx) {
+  if (!c) return set_err(BL_ERR_INVALID, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->ert.ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
+  if (frame_stride == 0) frame_stride = pitch * h;
+  TRY(check_frames(frames, pixel_type, n_frames, w, h, pitch, frame_stride));
+  if (n_boxes < 0 || n_boxes > (1 << 30)) return set_err(BL_ERR_INVALID, "bad box count");
+  if (n_boxes == 0) return BL_OK;
+  if (!boxes || !frame_of_box || !out_xy) return set_err(BL_ERR_INVALID, "null argument");
+  TRY(use_device(c));
+  // host-side validation of boxes (predict_landmarks' precondition, ert.cpp:101-102)
+  std::vector<bl_box> hb(n_boxes);
+  std::vector<int32_t> hf(n_boxes);
+  CK(cudaMemcpy(hb.data(), boxes, sizeof(bl_box) * n_boxes, cudaMemcpyDefault));
+  CK(cudaMemcpy(hf.data(), frame_of_box, sizeof(int32_t) * n_boxes, cudaMemcpyDefault));
+  for (int64_t i = 0; i < n_boxes; ++i) {
+    if (hb[i].w <= 0 || hb[i].h <= 0) return set_err(BL_ERR_INVALID, "predict_landmarks: face box must have positive area");
+    if (hf[i] < 0 || hf[i] >= n_frames) return set_err(BL_ERR_INVALID, "frame_of_box out of range");
+  }
+  timing_begin(c);
+  const void* dev = nullptr;
+  long long dp = 0, df = 0;
+  TRY(stage_input(c, c->ert_input, frames, pixel_type, n_frames, w, h, pitch, frame_stride, &dev, &dp, &df));
+  TRY(c->ert_boxes.ensure(sizeof(bl_box) * n_boxes));
+  TRY(c->ert_frames.ensure(sizeof(int32_t) * n_boxes));
+  TRY(c->ert_nfaces.ensure(sizeof(int)));
+  CK(cudaMemcpyAsync(c->ert_boxes.p, hb.data(), sizeof(bl_box) * n_boxes, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->ert_frames.p, hf.data(), sizeof(int32_t) * n_boxes, cudaMemcpyHostToDevice, c->st));
+  const int nf = (int)n_boxes;
+  CK(cudaMemcpyAsync(c->ert_nfaces.p, &nf, sizeof(int), cudaMemcpyHostToDevice, c->st));
+  uint8_t* leaf_dev = nullptr;
+  if (leaf_idx) {
+    TRY(c->ert_leaf.ensure((size_t)n_boxes * c->ert.dev.T * c->ert.dev.K + 1));
+    leaf_dev = c->ert_leaf.as<uint8_t>();
+  }
+  stage_mark(c, BL_STAGE_ERT);
+  TRY(run_ert(c, dev, pixel_type, w, h, dp, df, c->ert_frames.as<int>(), c->ert_boxes.as<int>(), 4,
+              c->ert_nfaces.as<int>(), nf, leaf_dev));
+  stage_mark(c, BL_STAGE_D2H);
+  CK(cudaMemcpyAsync(out_xy, c->ert_out.p, sizeof(double) * 2 * c->ert.dev.L * n_boxes, cudaMemcpyDefault, c->st));
+  if (leaf_idx)
+    CK(cudaMemcpyAsync(leaf_idx, leaf_dev, (size_t)n_boxes * c->ert.dev.T * c->ert.dev.K, cudaMemcpyDefault, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaGetLastError());
+  int err = 0;
+  CK(cudaMemcpy(&err, c->ert_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err == 1) return set_err(BL_ERR_INVALID, "similarity_transform: source shape has no spread");
+  if (err == 2) return set_err(BL_ERR_INVALID, "similarity_transform: target shape has no spread");
+  const int present[] = {BL_STAGE_H2D, BL_STAGE_ERT, BL_STAGE_D2H};
+  timing_end(c, present, 3);
+  return BL_OK;
+}
+
+// --------------------------------------------------------------- stage functions ----
+int bl_build_pyramid(bl_ctx* c, const void* image, int pix, int w, int h, int window, double* out, size_t out_cap,
+                     int* dims, double* scales, int max_levels, int* n_levels) {
+  if (!c || !image || !n_levels) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  TRY(check_frames(image, pix, 1, w, h, w, (size_t)w * h));
+  TRY(use_device(c));
+  std::vector<int> lw, lh;
+  pyramid_dims(w, h, window, lw, lh);
+  const int nl = (int)lw.size();
+  *n_levels = nl;
+  size_t total = 0;
+  std::vector<size_t> off(nl);
+  for (int k = 0; k < nl; ++k) {
+    off[k] = total;
+    total += (size_t)lw[k] * lh[k];
+    if (k < max_levels) {
+      if (dims) {
+        dims[2 * k] = lw[k];
+        dims[2 * k + 1] = lh[k];
+      }
+      if (scales) scales[k] = k == 0 ? 1.0 : std::pow(5.0 / 6.0, double(k));  // image.cpp:169
+    }
+  }
+  if (!out) return BL_OK;
+  if (out_cap < total) return set_err(BL_ERR_CAPACITY, "pyramid needs %zu doubles", total);
+  const size_t es = pix == BL_PIX_U8 ? 1 : 8;
+  const void* src = nullptr;
+  TRY(to_device(c, c->s_a, image, es * (size_t)w * h, &src));
+  TRY(c->s_b.ensure(sizeof(double) * total));
+  double* lv = c->s_b.as<double>();
+  const Launch L = launch_of(c);
+  if (pix == BL_PIX_U8) {
+    // level 0 as doubles (exact widening)
+    std::vector<uint8_t> tmp((size_t)w * h);
+    CK(cudaMemcpyAsync(tmp.data(), src, tmp.size(), cudaMemcpyDefault, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    std::vector<double> d(tmp.begin(), tmp.end());
+    CK(cudaMemcpyAsync(lv, d.data(), sizeof(double) * d.size(), cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  } else {
+    CK(cudaMemcpyAsync(lv, src, sizeof(double) * (size_t)w * h, cudaMemcpyDefault, c->st));
+  }
+  for (int k = 1; k < nl; ++k)
+    launch_resample(L, lv + off[k - 1], 0, lw[k - 1], lh[k - 1], lw[k - 1], (long long)lw[k - 1] * lh[k - 1],
+                    lv + off[k], lw[k], lh[k], (long long)lw[k] * lh[k], 1);
+  return from_device(c, out, lv, sizeof(double) * total);
+}
+
+int bl_downscale_bilinear(bl_ctx* c, const double* image, int w, int h, double* out) {
+  if (!c || !image || !out) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (w < 2 || h < 2) return set_err(BL_ERR_INVALID, "downscale_bilinear: output dimension would be 0");
+  TRY(use_device(c));
+  const int dw = w * 5 / 6, dh = h * 5 / 6;
+  const void* src = nullptr;
+  TRY(to_device(c, c->s_a, image, sizeof(double) * w * h, &src));
+  TRY(c->s_b.ensure(sizeof(double) * dw * dh));
+  launch_resample(launch_of(c), src, 0, w, h, w, (long long)w * h, c->s_b.as<double>(), dw, dh, (long long)dw * dh, 1);
+  return from_device(c, out, c->s_b.p, sizeof(double) * dw * dh);
+}
+
+int bl_compute_gradients(bl_ctx* c, const double* image, int w, int h, uint8_t* ori, double* mag) {
+  if (!c || !image || !ori || !mag) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (w < 3 || h < 3) return set_err(BL_ERR_INVALID, "compute_gradients: image must be at least 3x3");
+  TRY(use_device(c));
+  const void* src = nullptr;
+  TRY(to_device(c, c->s_a, image, sizeof(double) * w * h, &src));
+  TRY(c->s_b.ensure(sizeof(double) * w * h));
+  TRY(c->s_c.ensure((size_t)w * h));
+  launch_gradients(launch_of(c), (const double*)src, w, h, c->s_c.as<uint8_t>(), c->s_b.as<double>());
+  CK(cudaMemcpyAsync(ori, c->s_c.p, (size_t)w * h, cudaMemcpyDefault, c->st));
+  return from_device(c, mag, c->s_b.p, sizeof(double) * w * h);
+}
+
+int bl_histogramize(bl_ctx* c, const uint8_t* ori, const double* mag, int w, int h, double* bins) {
+  if (!c || !ori || !mag || !bins) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (w < 1 || h < 1) return set_err(BL_ERR_INVALID, "bad dims");
+  TRY(use_device(c));
+  const int cw = w / 8, ch = h / 8;
+  if (cw == 0 || ch == 0) return BL_OK;
+  const void *o = nullptr, *m = nullptr;
+  TRY(to_device(c, c->s_a, mag, sizeof(double) * w * h, &m));
+  TRY(to_device(c, c->s_c, ori, (size_t)w * h, &o));
+  PlanDesc H;
+  single_level_plan(H, w, h, cw, ch);
+  TRY(c->s_desc.ensure(sizeof(PlanDesc)));
+  CK(cudaMemcpyAsync(c->s_desc.p, &H, sizeof H, cudaMemcpyHostToDevice, c->st));
+  TRY(c->s_b.ensure(sizeof(double) * kBins * cw * ch));
+  launch_gradhist_field(launch_of(c), H, c->s_desc.as<PlanDesc>(), (const uint8_t*)o, (const double*)m,
+                        c->s_b.as<double>());
+  return from_device(c, bins, c->s_b.p, sizeof(double) * kBins * cw * ch);
+}
+
+int bl_cell_energy(bl_ctx* c, const double* bins, int cw, int ch, double* energy) {
+  if (!c || !bins || !energy) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (cw < 0 || ch < 0) return set_err(BL_ERR_INVALID, "bad dims");
+  TRY(use_device(c));
+  const long long cells = (long long)cw * ch;
+  if (cells == 0) return BL_OK;
+  const void* b = nullptr;
+  TRY(to_device(c, c->s_a, bins, sizeof(double) * kBins * cells, &b));
+  TRY(c->s_b.ensure(sizeof(double) * cells));
+  launch_energy(launch_of(c), (const double*)b, cells, c->s_b.as<double>());
+  return from_device(c, energy, c->s_b.p, sizeof(double) * cells);
+}
+
+int bl_compute_features(bl_ctx* c, const double* bins, const double* energy, int cw, int ch, double* features) {
+  if (!c || !bins || !energy || !features) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (cw < 0 || ch < 0) return set_err(BL_ERR_INVALID, "bad dims");
+  TRY(use_device(c));
+  const long long cells = (long long)cw * ch;
+  if (cells == 0) return BL_OK;
+  const void *b = nullptr, *e = nullptr;
+  TRY(to_device(c, c->s_a, bins, sizeof(double) * kBins * cells, &b));
+  TRY(to_device(c, c->s_b, energy, sizeof(double) * cells, &e));
+  PlanDesc H;
+  single_level_plan(H, cw * 8, ch * 8, cw, ch);
+  TRY(c->s_desc.ensure(sizeof(PlanDesc)));
+  CK(cudaMemcpyAsync(c->s_desc.p, &H, sizeof H, cudaMemcpyHostToDevice, c->st));
+  TRY(c->s_c.ensure(sizeof(double) * kFeat * cells));
+  launch_features(launch_of(c), H, c->s_desc.as<PlanDesc>(), (const double*)b, (const double*)e,
+                  c->s_c.as<double>(), nullptr);
+  return from_device(c, features, c->s_c.p, sizeof(double) * kFeat * cells);
+}
+
+int bl_extract_features(bl_ctx* c, const double* image, int w, int h, double* features, double* bins,
+                        double* energy) {
+  if (!c || !image || !features) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (w < 3 || h < 3) return set_err(BL_ERR_INVALID, "compute_gradients: image must be at least 3x3");
+  TRY(use_device(c));
+  const int cw = w / 8, ch = h / 8;
+  const long long cells = (long long)cw * ch;
+  if (cells == 0) return BL_OK;
+  const void* src = nullptr;
+  TRY(to_device(c, c->s_a, image, sizeof(double) * w * h, &src));
+  PlanDesc H;
+  single_level_plan(H, w, h, cw, ch);
+  TRY(c->s_desc.ensure(sizeof(PlanDesc)));
+  CK(cudaMemcpyAsync(c->s_desc.p, &H, sizeof H, cudaMemcpyHostToDevice, c->st));
+  TRY(c->s_b.ensure(sizeof(double) * kBins * cells));
+  TRY(c->s_c.ensure(sizeof(double) * cells));
+  TRY(c->s_d.ensure(sizeof(double) * kFeat * cells));
+  const Launch L = launch_of(c);
+  launch_gradhist_levels(L, H, c->s_desc.as<PlanDesc>(), 0, 1, src, 1, c->s_b.as<double>(), c->s_c.as<double>());
+  launch_features(L, H, c->s_desc.as<PlanDesc>(), c->s_b.as<double>(), c->s_c.as<double>(), c->s_d.as<double>(),
+                  nullptr);
+  if (bins) CK(cudaMemcpyAsync(bins, c->s_b.p, sizeof(double) * kBins * cells, cudaMemcpyDefault, c->st));
+  if (energy) CK(cudaMemcpyAsync(energy, c->s_c.p, sizeof(double) * cells, cudaMemcpyDefault, c->st));
+  return from_device(c, features, c->s_d.p, sizeof(double) * kFeat * cells);
+}
+
+int bl_score_window(bl_ctx* c, const double* features, int cw, int ch, const double* weights, double bias,
+                    double* scores) {
+  if (!c || !features || !weights || !scores) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (cw < kWin || ch < kWin) return set_err(BL_ERR_INVALID, "feature image smaller than the 10x10 detection window");
+  TRY(use_device(c));
+  const long long cells = (long long)cw * ch;
+  const long long n = (long long)(cw - 9) * (ch - 9);
+  const void *f = nullptr, *wt = nullptr;
+  TRY(to_device(c, c->s_a, features, sizeof(double) * kFeat * cells, &f));
+  TRY(to_device(c, c->s_b, weights, sizeof(double) * kFilterW, &wt));
+  TRY(c->s_c.ensure(sizeof(double) * n));
+  launch_score_exact_all(launch_of(c), (const double*)f, cw, ch, (const double*)wt, bias, c->s_c.as<double>());
+  return from_device(c, scores, c->s_c.p, sizeof(double) * n);
+}
+
+int bl_nms(bl_ctx* c, const bl_detection* dets, int64_t n, double iou_threshold, bl_detection* out, int64_t* kept) {
+  if (!c || (!dets && n > 0) || !out || !kept) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  *kept = 0;
+  if (n <= 0) return BL_OK;
+  if (n > (1ll << 26)) return set_err(BL_ERR_CAPACITY, "too many detections");
+  TRY(use_device(c));
+  TRY(c->s_a.ensure(sizeof(bl_detection) * n));
+  TRY(c->s_b.ensure(sizeof(bl_detection) * n));
+  TRY(c->s_c.ensure(sizeof(int) * 2));
+  const long long gk = nms_gkeys_per_frame(n);
+  if (gk) TRY(c->s_d.ensure(nms_key_bytes() * gk));
+  CK(cudaMemcpyAsync(c->s_a.p, dets, sizeof(bl_detection) * n, cudaMemcpyDefault, c->st));
+  const int cnt = (int)n;
+  CK(cudaMemcpyAsync(c->s_c.p, &cnt, sizeof(int), cudaMemcpyHostToDevice, c->st));
+  launch_nms(launch_of(c), c->s_a.as<DevDet>(), c->s_c.as<int>(), n, 1, iou_threshold, c->s_b.as<DevDet>(),
+             c->s_c.as<int>() + 1, c->s_d.p, gk);
+  int k = 0;
+  CK(cudaMemcpyAsync(&k, c->s_c.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  *kept = k;
+  return from_device(c, out, c->s_b.p, sizeof(bl_detection) * k);
+}
+
+int bl_orientation_bins(bl_ctx* c, const double* gx, const double* gy, int64_t n, uint8_t* bins) {
+  if (!c || !gx || !gy || !bins) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (n <= 0) return BL_OK;
+  TRY(use_device(c));
+  const void *a = nullptr, *b = nullptr;
+  TRY(to_device(c, c->s_a, gx, sizeof(double) * n, &a));
+  TRY(to_device(c, c->s_b, gy, sizeof(double) * n, &b));
+  TRY(c->s_c.ensure((size_t)n));
+  launch_orientation(launch_of(c), (const double*)a, (const double*)b, n, c->s_c.as<uint8_t>());
+  return from_device(c, bins, c->s_c.p, (size_t)n);
+}
+
+}  // extern "C"

@@ -1,0 +1,294 @@
+// Classifier stage 2 (exact re-score), threshold + box mapping, and per-frame NMS.
+//
+// Compiled with --fmad=false.  The re-score evaluates a candidate window exactly as
+// score_separable does (detector.cpp:66-100): for each window row j the 310-term dot
+// product of the feature strip at (cx, cy+j) with filter row j, accumulated in order
+// without FMA, then the 10 row sums in order, then + bias.  Detections therefore carry
+// bit-identical scores, and threshold_detections' box mapping (detector.cpp:102-122) and
+// NMS (detector.cpp:124-142, IoU detector.cpp:16-28) are replayed with the same double
+// operations, so the kept list is bit-identical to the reference's.
+#include <float.h>
+
+#include "bl_internal.cuh"
+
+namespace blb {
+
+// Exact separable window score; lanes 0..9 each own one window row.  Result valid in lane 0.
+BL_DEV double exact_window_score(const double* __restrict__ feat, int cw, int cx, int cy,
+                                 const double* __restrict__ w, double bias, int lane) {
+  double acc = 0.0;
+  if (lane < kWin) {
+    const double* strip = feat + ((long long)(cy + lane) * cw + cx) * kFeat;
+    const double* wr = w + lane * kRowW;
+#pragma unroll 10
+    for (int k = 0; k < kRowW; ++k) acc = dadd(acc, dmul(__ldg(strip + k), __ldg(wr + k)));
+  }
+  double total = 0.0;
+#pragma unroll
+  for (int j = 0; j < kWin; ++j) total = dadd(total, __shfl_sync(0xffffffffu, acc, j));
+  return dadd(total, bias);
+}
+
+BL_DEV int round_half_up(double v) { return (int)floor(dadd(v, 0.5)); }  // detector.cpp:41
+
+__global__ void __launch_bounds__(256) k_rescore(const PlanDesc* __restrict__ P,
+                                                 const double* __restrict__ feat64,
+                                                 const double* __restrict__ w64,
+                                                 const double* __restrict__ bias, double thr,
+                                                 int cell_px, const Candidate* __restrict__ cand,
+                                                 const unsigned long long* __restrict__ n_cand,
+                                                 long long cand_cap, DevDet* __restrict__ dets,
+                                                 int* __restrict__ det_count, long long cap_pf,
+                                                 int* __restrict__ overflow) {
+  const int lane = threadIdx.x & 31;
+  const long long n = min((long long)*n_cand, cand_cap);
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+    const Candidate c = cand[i];
+    const int s = c.slot_r >> 3, r = c.slot_r & 7;
+    const LevelDesc& D = P->lv[s];
+    const double* fb = feat64 + (D.cell_off + (long long)c.frame * D.cw * D.ch) * kFeat;
+    const double sc = exact_window_score(fb, D.cw, c.cx, c.cy, w64 + r * kFilterW, bias[r], lane);
+    if (lane == 0 && sc > thr) {  // detector.cpp:110 (strict)
+      DevDet d;
+      d.x = round_half_up(ddiv((double)(c.cx * cell_px), D.c));
+      d.y = round_half_up(ddiv((double)(c.cy * cell_px), D.c));
+      d.w = D.side;
+      d.h = D.side;
+      d.score = sc;
+      d.scale_index = D.level;
+      d.rotation_index = r;
+      const int idx = atomicAdd(det_count + c.frame, 1);
+      if (idx < cap_pf)
+        dets[(long long)c.frame * cap_pf + idx] = d;
+      else
+        atomicExch(overflow, 1);
+    }
+  }
+}
+
+void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, const double* w64,
+                    const double* bias, double thr, int cell_px, const Candidate* cand,
+                    const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
+                    int* det_count, long long cap_pf, int* overflow, int blocks) {
+  k_rescore<<<blocks, 256, 0, L.st>>>(Pd, feat64, w64, bias, thr, cell_px, cand, n_cand, cand_cap,
+                                      dets, det_count, cap_pf, overflow);
+  ++*L.counter;
+}
+
+// Every anchor of one feature image, one filter: bl_score_window (score_separable).
+__global__ void __launch_bounds__(256) k_score_all(const double* __restrict__ feat, int cw, int ch,
+                                                   const double* __restrict__ w, double bias,
+                                                   double* __restrict__ scores) {
+  const int lane = threadIdx.x & 31;
+  const int sw = cw - (kWin - 1), sh = ch - (kWin - 1);
+  const long long n = (long long)sw * sh;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+    const int cy = (int)(i / sw), cx = (int)(i - (long long)(i / sw) * sw);
+    const double sc = exact_window_score(feat, cw, cx, cy, w, bias, lane);
+    if (lane == 0) scores[i] = sc;
+  }
+}
+
+void launch_score_exact_all(const Launch& L, const double* feat64, int cw, int ch, const double* w64,
+                            double bias, double* scores) {
+  const long long n = (long long)(cw - 9) * (ch - 9);
+  if (n <= 0) return;
+  const int blocks = (int)min(div_up(n, 8), (long long)148 * 16);
+  k_score_all<<<blocks, 256, 0, L.st>>>(feat64, cw, ch, w64, bias, scores);
+  ++*L.counter;
+}
+
+// ------------------------------------------------------------------------- NMS ----
+// detector.cpp:16-28
+BL_DEV double iou_exact(const DevDet& a, const DevDet& b) {
+  const long long ix0 = max(a.x, b.x);
+  const long long iy0 = max(a.y, b.y);
+  const long long ix1 = min((long long)(a.x + a.w), (long long)(b.x + b.w));
+  const long long iy1 = min((long long)(a.y + a.h), (long long)(b.y + b.h));
+  const long long iw = ix1 - ix0;
+  const long long ih = iy1 - iy0;
+  if (iw <= 0 || ih <= 0) return 0.0;
+  const double inter = dmul((double)iw, (double)ih);
+  const double uni = dsub(dadd(dmul((double)a.w, (double)a.h), dmul((double)b.w, (double)b.h)), inter);
+  if (uni <= 0.0) return 0.0;
+  return ddiv(inter, uni);
+}
+
+struct NmsKey {
+  double score;
+  unsigned long long t1, t2;  // (y, x) and (scale, rotation), sign-flipped for unsigned order
+  int idx;
+  int pad;
+};
+
+// detector.cpp:125-129: score descending, then (y, x, scale_index, rotation_index) ascending.
+BL_DEV bool before(const NmsKey& a, const NmsKey& b) {
+  if (a.score != b.score) return a.score > b.score;
+  if (a.t1 != b.t1) return a.t1 < b.t1;
+  if (a.t2 != b.t2) return a.t2 < b.t2;
+  return a.idx < b.idx;
+}
+
+BL_DEV unsigned long long pack2(int hi, int lo) {
+  return ((unsigned long long)((unsigned)hi ^ 0x80000000u) << 32) | (unsigned)(lo ^ 0x80000000);
+}
+
+constexpr int kNmsSmemKeys = 2048;   // keys sorted in shared memory up to this count
+constexpr int kNmsSmemKept = 1024;   // kept boxes cached in shared memory
+
+// One CTA per frame: bitonic sort of the frame's detections, then the greedy scan by
+// warp 0 (kept boxes checked 32 at a time with __any_sync).
+__global__ void __launch_bounds__(256) k_nms(const DevDet* __restrict__ dets,
+                                             const int* __restrict__ det_count, long long cap_pf,
+                                             double iou_thr, DevDet* __restrict__ kept_out,
+                                             int* __restrict__ kept_count, NmsKey* __restrict__ gkeys,
+                                             long long gkeys_pf) {
+  extern __shared__ unsigned char nms_smem[];
+  const int f = blockIdx.x;
+  const int n = (int)min((long long)det_count[f], cap_pf);
+  const DevDet* D = dets + (long long)f * cap_pf;
+  if (n == 0) {
+    if (threadIdx.x == 0) kept_count[f] = 0;
+    return;
+  }
+  int Pn = 1;
+  while (Pn < n) Pn <<= 1;
+  NmsKey* keys = Pn <= kNmsSmemKeys ? reinterpret_cast<NmsKey*>(nms_smem) : gkeys + (long long)f * gkeys_pf;
+  DevDet* kept_s = reinterpret_cast<DevDet*>(nms_smem + sizeof(NmsKey) * kNmsSmemKeys);
+  for (int i = threadIdx.x; i < Pn; i += blockDim.x) {
+    NmsKey k;
+    if (i < n) {
+      const DevDet d = D[i];
+      k.score = d.score;
+      k.t1 = pack2(d.y, d.x);
+      k.t2 = pack2(d.scale_index, d.rotation_index);
+      k.idx = i;
+    } else {
+      k.score = -DBL_MAX;
+      k.t1 = k.t2 = ~0ull;
+      k.idx = 0x7fffffff;
+    }
+    k.pad = 0;
+    keys[i] = k;
+  }
+  __syncthreads();
+  for (int k = 2; k <= Pn; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < Pn; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const NmsKey a = keys[i], b = keys[ixj];
+          const bool up = (i & k) == 0;
+          if (up ? before(b, a) : before(a, b)) {
+            keys[i] = b;
+            keys[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  DevDet* out = kept_out + (long long)f * cap_pf;
+  int kept = 0;
+  for (int i = 0; i < n; ++i) {
+    const DevDet d = D[keys[i].idx];
+    bool sup = false;
+    for (int k = lane; k < kept; k += 32) {
+      const DevDet kb = k < kNmsSmemKept ? kept_s[k] : out[k];
+      if (iou_exact(d, kb) > iou_thr) sup = true;  // detector.cpp:134
+    }
+    if (!__any_sync(0xffffffffu, sup)) {
+      if (lane == 0) {
+        out[kept] = d;
+        if (kept < kNmsSmemKept) kept_s[kept] = d;
+      }
+      ++kept;
+      __syncwarp();
+    }
+  }
+  if (lane == 0) kept_count[f] = kept;
+}
+
+size_t nms_smem_bytes() { return sizeof(NmsKey) * kNmsSmemKeys + sizeof(DevDet) * kNmsSmemKept; }
+
+long long nms_gkeys_per_frame(long long cap_pf) {
+  long long p = 1;
+  while (p < cap_pf) p <<= 1;
+  return p > kNmsSmemKeys ? p : 0;
+}
+
+size_t nms_key_bytes() { return sizeof(NmsKey); }
+
+void launch_nms(const Launch& L, const DevDet* dets, const int* det_count, long long cap_pf, int n_frames,
+                double iou_thr, DevDet* kept_out, int* kept_count, void* gkeys, long long gkeys_pf) {
+  if (n_frames <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_nms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nms_smem_bytes());
+    attr = true;
+  }
+  k_nms<<<n_frames, 256, nms_smem_bytes(), L.st>>>(dets, det_count, cap_pf, iou_thr, kept_out, kept_count,
+                                                   (NmsKey*)gkeys, gkeys_pf);
+  ++*L.counter;
+}
+
+// ------------------------------------------------- kept detections -> flat face list ----
+// One CTA: prefix sum of kept counts (frame order), then every kept detection is copied to a
+// flat array (the order a sequential per-frame loop produces) together with its frame index.
+__global__ void __launch_bounds__(1024) k_flatten(const DevDet* __restrict__ kept,
+                                                  const int* __restrict__ kept_count, long long cap_pf,
+                                                  int n_frames, int* __restrict__ offsets,
+                                                  DevDet* __restrict__ flat, int* __restrict__ face_frame,
+                                                  int* __restrict__ n_faces, long long flat_cap) {
+  __shared__ int s_part[1024];
+  const int tid = threadIdx.x;
+  // each thread scans a contiguous chunk of frames
+  const int per = (n_frames + blockDim.x - 1) / blockDim.x;
+  const int f0 = min(n_frames, tid * per), f1 = min(n_frames, f0 + per);
+  int sum = 0;
+  for (int f = f0; f < f1; ++f) sum += kept_count[f];
+  s_part[tid] = sum;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const int v = tid >= o ? s_part[tid - o] : 0;
+    __syncthreads();
+    s_part[tid] += v;
+    __syncthreads();
+  }
+  int run = s_part[tid] - sum;
+  for (int f = f0; f < f1; ++f) {
+    offsets[f] = run;
+    run += kept_count[f];
+  }
+  if (tid == blockDim.x - 1) {
+    offsets[n_frames] = s_part[tid];
+    *n_faces = s_part[tid];
+  }
+  __syncthreads();
+  // copy: warp per frame
+  const int lane = tid & 31;
+  for (int f = tid >> 5; f < n_frames; f += blockDim.x >> 5) {
+    const int c = kept_count[f];
+    const int o = offsets[f];
+    for (int k = lane; k < c; k += 32) {
+      if (o + k < flat_cap) {
+        flat[o + k] = kept[(long long)f * cap_pf + k];
+        face_frame[o + k] = f;
+      }
+    }
+  }
+}
+
+void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, long long cap_pf,
+                    int n_frames, int* offsets, DevDet* flat, int* face_frame, int* n_faces,
+                    long long flat_cap) {
+  k_flatten<<<1, 1024, 0, L.st>>>(kept, kept_count, cap_pf, n_frames, offsets, flat, face_frame, n_faces,
+                                  flat_cap);
+  ++*L.counter;
+}
+
+}  // namespace blb

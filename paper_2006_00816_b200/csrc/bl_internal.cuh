@@ -1,0 +1,156 @@
+// Internal definitions shared by the blinkline_b200 kernels and the C-ABI host code.
+//
+// Exactness policy: every stage whose result the reference defines to the
+// last bit -- resample, gradient/orientation, histogram, energy, features, the exact
+// re-score, IoU, ERT traversal/accumulation -- lives in a translation unit compiled with
+// --fmad=false and spells its double arithmetic with the _rn intrinsics in the reference's
+// evaluation order.  Only the fp32 screening classifier (bl_classify.cu) is compiled with
+// FMA contraction; its results never reach the output without an exact fp64 re-score.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/blinkline_b200.h"
+
+namespace blb {
+
+constexpr int kBins = 18;
+constexpr int kFeat = 31;
+constexpr int kFeatPad = 32;     // fp32 planar feature planes (31 real + 1 zero plane)
+constexpr int kWin = 10;         // window cells (the reference's scorer is fixed at 10x10x31)
+constexpr int kRowW = kWin * kFeat;  // 310 weights per window row
+constexpr int kFilterW = kWin * kRowW;  // 3100
+constexpr int kFilters = 5;
+constexpr int kMaxLevels = 32;
+
+// Screening tile: a warp scores a 32 x 4 block of anchors (8 lanes x 4 anchors along x,
+// 4 rows), all 5 filters.  Feature planes are padded so its float4 loads never go out of
+// bounds.
+constexpr int kTileAX = 32;
+constexpr int kTileAY = 4;
+
+// gradHist: a warp owns 31 cells of a cell row strip and kCellRows cell rows.
+constexpr int kGhCells = 31;
+constexpr int kGhRows = 4;
+
+struct LevelDesc {
+  int w, h;              // level pixel dims
+  int cw, ch;            // cells (w/8, h/8)
+  int sw, sh;            // anchors (cw-9, ch-9)
+  int level;             // pyramid level index k
+  int side;              // round_half_up(window_px / c)
+  double c;              // (5/6)^k from the host's libm pow (detector.cpp:104)
+  long long pix_off;     // level pixels: element offset of frame 0 in the level arena
+  long long pix_fstride; // elements between frames
+  int pix_pitch;         // elements between rows
+  long long cell_off;    // cells: offset of frame 0 in the cell arenas (bins/energy/feat64)
+  long long f32_off;     // fp32 planar features: float offset of frame 0
+  int cw_pad, ch_pad;    // fp32 planar plane dims
+  long long f32_fstride; // floats between frames (= 32 * ch_pad * cw_pad)
+  // work decomposition (block ranges are global across levels)
+  int gh_tiles_x, gh_tiles_y;  // gradHist warp tiles per frame
+  long long gh_begin;          // first gradHist warp-tile id of this level
+  int sc_tiles_x, sc_tiles_y;  // screening warp tiles per frame
+  long long sc_begin;          // first screening warp-tile id of this level
+  long long cell_begin;        // first cell id (for per-cell kernels) of this level
+  long long anchor_base;       // per-frame anchor offset (for candidate records)
+};
+
+struct PlanDesc {
+  int n_frames;
+  int n_scored;                // scored levels (eligible and >= one window)
+  LevelDesc lv[kMaxLevels];
+  long long gh_total;          // total gradHist warp tiles
+  long long sc_total;          // total screening warp tiles
+  long long cell_total;        // total cells over levels and frames
+  long long cells_per_frame;
+};
+
+// Candidate from the fp32 screen: (frame, scored-level slot, filter, cx, cy).
+struct Candidate {
+  int frame;
+  int slot_r;   // slot * 8 + r
+  int cx, cy;
+};
+
+// Raw detection record on the device (same layout as bl_detection).
+struct DevDet {
+  int x, y, w, h;
+  double score;
+  int scale_index, rotation_index;
+};
+static_assert(sizeof(DevDet) == sizeof(bl_detection), "layout");
+
+struct ErtDev {
+  int L, T, K, F, S, NL;
+  double shrinkage;
+  const double* mean_xy;      // L*2
+  const int16_t* anchors;     // T*K*S*2
+  const double* split;        // T*K*S*5
+  const double* leaves;       // T*K*NL*L*2
+  double mean_cx, mean_cy;    // centroid of the mean shape (host-computed, ert.cpp:33-43 order)
+};
+
+// ----------------------------------------------------------------- helpers ------
+__host__ __device__ inline long long div_up(long long a, long long b) { return (a + b - 1) / b; }
+
+#define BL_DEV __device__ __forceinline__
+
+// Exact double ops, never contracted (these TUs are also compiled with --fmad=false).
+BL_DEV double dadd(double a, double b) { return __dadd_rn(a, b); }
+BL_DEV double dsub(double a, double b) { return __dsub_rn(a, b); }
+BL_DEV double dmul(double a, double b) { return __dmul_rn(a, b); }
+BL_DEV double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ------------------------------------------------------------- host launchers ----
+// Defined in the kernel TUs, called by bl_capi.cu.  All are asynchronous on `L.st`;
+// `Pd` is the device copy of the host plan `Ph`.
+struct Launch {
+  cudaStream_t st;
+  uint64_t* counter;  // incremented per kernel launch
+};
+
+// bl_pyramid.cu
+void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
+                     long long s_fstride, double* dst, int dw, int dh, long long d_fstride, int n);
+// bl_hog.cu
+void set_direction_table(const double* ux, const double* uy);
+void launch_gradhist_levels(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, int s_lo,
+                            int s_hi, const void* base, int src_kind /*0 u8, 1 f64*/, double* bins,
+                            double* energy);
+void launch_gradhist_field(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd,
+                           const uint8_t* ori, const double* mag, double* bins);
+void launch_gradients(const Launch& L, const double* img, int w, int h, uint8_t* ori, double* mag);
+void launch_orientation(const Launch& L, const double* gx, const double* gy, long long n, uint8_t* out);
+void launch_energy(const Launch& L, const double* bins, long long cells, double* energy);
+void launch_features(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, const double* bins,
+                     const double* energy, double* feat64, float* feat32);
+// bl_classify.cu
+void launch_screen(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, const float* feat32,
+                   const float* w32, const float* cut, Candidate* cand, unsigned long long* n_cand,
+                   long long cand_cap);
+// bl_exact.cu
+void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, const double* w64,
+                    const double* bias, double thr, int cell_px, const Candidate* cand,
+                    const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
+                    int* det_count, long long cap_pf, int* overflow, int blocks);
+void launch_score_exact_all(const Launch& L, const double* feat64, int cw, int ch, const double* w64,
+                            double bias, double* scores);
+size_t nms_key_bytes();
+long long nms_gkeys_per_frame(long long cap_pf);
+void launch_nms(const Launch& L, const DevDet* dets, const int* det_count, long long cap_pf, int n_frames,
+                double iou_thr, DevDet* kept_out, int* kept_count, void* gkeys, long long gkeys_pf);
+void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, long long cap_pf,
+                    int n_frames, int* offsets, DevDet* flat, int* face_frame, int* n_faces,
+                    long long flat_cap);
+// bl_ert.cu
+void launch_ert_init(const Launch& L, const ErtDev& M, const int* n_faces, int cap, double* cur);
+void launch_ert_level(const Launch& L, const ErtDev& M, int t, const void* frames, int u8, int w, int h,
+                      long long pitch, long long fstride, const int* face_frame, const int* boxes,
+                      int box_stride, const int* n_faces, int cap, double* cur, uint8_t* leaf_idx,
+                      int* err, int blocks);
+void launch_ert_finish(const Launch& L, const ErtDev& M, const int* boxes, int box_stride,
+                       const int* n_faces, int cap, const double* cur, double* out_xy);
+
+}  // namespace blb
