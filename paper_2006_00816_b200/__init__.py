@@ -224,7 +224,7 @@ class Context:
         a, pix, n, h, w = _frames(frames)
         cap = cap or max(1024, 64 * n)
         while True:
-            out = np.zeros(cap, DET_DTYPE)
+            out = np.empty(cap, DET_DTYPE)
             counts = np.zeros(n, np.int32)
             total = C.c_int64(0)
             rc = lib.bl_detect(self._h, _addr(a), pix, n, w, h, w, w * h, out.ctypes.data, cap,
@@ -242,8 +242,8 @@ class Context:
         a, pix, n, h, w = _frames(frames)
         cap = cap or max(1024, 64 * n)
         while True:
-            out = np.zeros(cap, DET_DTYPE)
-            lm = np.zeros((cap, self.ert_L or 1, 2))
+            out = np.empty(cap, DET_DTYPE)
+            lm = np.empty((cap, self.ert_L or 1, 2))
             counts = np.zeros(n, np.int32)
             total = C.c_int64(0)
             rc = lib.bl_detect_landmarks(self._h, _addr(a), pix, n, w, h, w, w * h, out.ctypes.data, cap,

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -263,7 +264,7 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
     L.f32_fstride = (long long)kFeatPad * L.ch_pad * L.cw_pad;
     f32 += (long long)n * L.f32_fstride;
     L.gh_tiles_x = (int)div_up(L.cw, kGhCells);
-    L.gh_tiles_y = (int)div_up(L.ch, kGhRows);
+    L.gh_tiles_y = (int)div_up(L.ch, kGhSegRows);
     L.gh_begin = gh;
     gh += (long long)n * L.gh_tiles_x * L.gh_tiles_y;
     L.sc_tiles_x = (int)div_up(L.sw, kTileAX);
@@ -564,7 +565,7 @@ void single_level_plan(PlanDesc& H, int w, int h, int cw, int ch) {
   L.pix_pitch = w;
   L.pix_fstride = (long long)w * h;
   L.gh_tiles_x = (int)div_up(cw, kGhCells);
-  L.gh_tiles_y = (int)div_up(ch, kGhRows);
+  L.gh_tiles_y = (int)div_up(ch, kGhSegRows);
   H.gh_total = (long long)L.gh_tiles_x * L.gh_tiles_y;
   H.cell_total = (long long)cw * ch;
   H.cells_per_frame = H.cell_total;

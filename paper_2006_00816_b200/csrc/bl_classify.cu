@@ -23,7 +23,9 @@ namespace blb {
 constexpr int kWBlock = 52;  // per (window row j, feature f): 10 cells x 5 filters, padded to 13 float4
 constexpr int kScreenSmem = kWin * kFeat * kWBlock * (int)sizeof(float);  // 64,480 B
 
-__global__ void __launch_bounds__(128) k_screen(const PlanDesc* __restrict__ P,
+constexpr int kScreenWarps = 8;  // warps per CTA sharing one smem copy of the weights
+
+__global__ void __launch_bounds__(kScreenWarps * 32, 2) k_screen(const PlanDesc* __restrict__ P,
                                                 const float* __restrict__ feat32,
                                                 const float* __restrict__ w32,
                                                 const float* __restrict__ cut,
@@ -37,7 +39,7 @@ __global__ void __launch_bounds__(128) k_screen(const PlanDesc* __restrict__ P,
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long wid = (long long)blockIdx.x * 4 + warp;
+  const long long wid = (long long)blockIdx.x * kScreenWarps + warp;
   if (wid >= total) return;
   int s = 0;
   while (s + 1 < P->n_scored && wid >= P->lv[s + 1].sc_begin) ++s;
@@ -58,6 +60,11 @@ __global__ void __launch_bounds__(128) k_screen(const PlanDesc* __restrict__ P,
 #pragma unroll
     for (int r = 0; r < kFilters; ++r) acc[q][r] = 0.f;
 
+  // software pipeline: the next (j, f) feature vectors are in flight while the current
+  // ones feed 200 FMAs
+  const float* rowp0 = fb + (long long)y * cw_pad;
+  float4 n0 = __ldg(reinterpret_cast<const float4*>(rowp0)), n1 = __ldg(reinterpret_cast<const float4*>(rowp0) + 1),
+         n2 = __ldg(reinterpret_cast<const float4*>(rowp0) + 2), n3 = __ldg(reinterpret_cast<const float4*>(rowp0) + 3);
 #pragma unroll 1
   for (int j = 0; j < kWin; ++j) {
     float aj[4][kFilters];
@@ -65,14 +72,20 @@ __global__ void __launch_bounds__(128) k_screen(const PlanDesc* __restrict__ P,
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int r = 0; r < kFilters; ++r) aj[q][r] = 0.f;
-    const float* rowp = fb + (long long)(y + j) * cw_pad;
     const float4* wj = sW4 + j * kFeat * (kWBlock / 4);
 #pragma unroll 1
     for (int ff = 0; ff < kFeat; ++ff) {
-      const float4* p = reinterpret_cast<const float4*>(rowp + ff * plane);
-      const float4 a0 = __ldg(p), a1 = __ldg(p + 1), a2 = __ldg(p + 2), a3 = __ldg(p + 3);
-      const float v[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
-                           a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
+      const float v[16] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w,
+                           n2.x, n2.y, n2.z, n2.w, n3.x, n3.y, n3.z, n3.w};
+      {  // prefetch (j, ff+1), or (j+1, 0); the last prefetch re-reads row y+9, harmlessly
+        const int nf = ff + 1 < kFeat ? ff + 1 : 0;
+        const int nj = ff + 1 < kFeat ? j : min(j + 1, kWin - 1);
+        const float4* p = reinterpret_cast<const float4*>(fb + (long long)(y + nj) * cw_pad + nf * plane);
+        n0 = __ldg(p);
+        n1 = __ldg(p + 1);
+        n2 = __ldg(p + 2);
+        n3 = __ldg(p + 3);
+      }
       const float4* wp = wj + ff * (kWBlock / 4);
       float wv[kWBlock];
 #pragma unroll
@@ -147,7 +160,7 @@ void launch_screen(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, cons
     cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, kScreenSmem);
     attr = true;
   }
-  k_screen<<<(unsigned)div_up(Ph.sc_total, 4), 128, kScreenSmem, L.st>>>(Pd, feat32, w32, cut, cand,
+  k_screen<<<(unsigned)div_up(Ph.sc_total, kScreenWarps), kScreenWarps * 32, kScreenSmem, L.st>>>(Pd, feat32, w32, cut, cand,
                                                                         n_cand, cand_cap, Ph.sc_total);
   ++*L.counter;
 }

@@ -30,9 +30,9 @@ constexpr int kMaxLevels = 32;
 constexpr int kTileAX = 32;
 constexpr int kTileAY = 4;
 
-// gradHist: a warp owns 31 cells of a cell row strip and kCellRows cell rows.
+// gradHist: a warp owns 31 cells of a cell-row strip over a segment of kGhSegRows cell rows.
 constexpr int kGhCells = 31;
-constexpr int kGhRows = 4;
+constexpr int kGhSegRows = 12;
 
 struct LevelDesc {
   int w, h;              // level pixel dims
