@@ -162,6 +162,10 @@ int bl_nms(bl_ctx* ctx, const bl_detection* dets, int64_t n, double iou_threshol
 /* Device orientation argmax on explicit (gx, gy) pairs (hog.cpp:41-49 semantics). */
 int bl_orientation_bins(bl_ctx* ctx, const double* gx, const double* gy, int64_t n, uint8_t* bins);
 
+/* Self-check of the device gradient-magnitude square root (sqrt_fast, bl_hog.cu) against
+ * IEEE __dsqrt_rn on the same inputs (inputs in [1e-300, 1e300]). */
+int bl_debug_sqrt(bl_ctx* ctx, const double* in, int64_t n, double* fast, double* ieee);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,6 +95,7 @@ _SIGS = {
     "bl_score_window": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _dbl, _vp]),
     "bl_nms": (C.c_int, [_vp, _vp, _i64, _dbl, _vp, _P(_i64)]),
     "bl_orientation_bins": (C.c_int, [_vp, _vp, _vp, _i64, _vp]),
+    "bl_debug_sqrt": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)
@@ -356,6 +357,12 @@ class Context:
         _err(lib.bl_nms(self._h, dets.ctypes.data if len(dets) else None, len(dets), float(iou_threshold),
                         out.ctypes.data, C.byref(kept)))
         return out[:kept.value].copy()
+
+    def debug_sqrt(self, x):
+        x = _np(x, np.float64).ravel()
+        fast, ieee = np.zeros_like(x), np.zeros_like(x)
+        _err(lib.bl_debug_sqrt(self._h, x.ctypes.data, len(x), fast.ctypes.data, ieee.ctypes.data))
+        return fast, ieee
 
     def orientation_bins(self, gx, gy):
         gx = _np(gx, np.float64).ravel()

@@ -136,7 +136,7 @@ struct Plan {
   long long cand_cap = 0;
   long long f32_elems = 0;
   long long gkeys_pf = 0;
-  DevBuf arena, bins, energy, feat64, feat32, cand, n_cand, dets, det_count, kept, kept_count, gkeys,
+  DevBuf arena, fmag, fori, bins, energy, feat64, feat32, cand, n_cand, dets, det_count, kept, kept_count, gkeys,
       overflow, offsets, flat, face_frame, n_faces, input;
 };
 
@@ -233,7 +233,7 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
   std::memset(&H, 0, sizeof H);
   H.n_frames = n;
   H.n_scored = (int)P.scored.size();
-  long long cells = 0, gh = 0, sc = 0, f32 = 0, anchors_pf = 0;
+  long long cells = 0, gh = 0, sc = 0, f32 = 0, anchors_pf = 0, fld = 0, gr = 0;
   for (int s = 0; s < H.n_scored; ++s) {
     const int k = P.scored[s];
     LevelDesc& L = H.lv[s];
@@ -263,6 +263,12 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
     L.f32_off = f32;
     L.f32_fstride = (long long)kFeatPad * L.ch_pad * L.cw_pad;
     f32 += (long long)n * L.f32_fstride;
+    L.fld_off = fld;
+    fld += (long long)n * L.w * L.h;
+    L.gr_tiles_x = (int)div_up(L.w, 32);
+    L.gr_tiles_y = (int)div_up(L.h, 32);
+    L.gr_begin = gr;
+    gr += (long long)n * L.gr_tiles_x * L.gr_tiles_y;
     L.gh_tiles_x = (int)div_up(L.cw, kGhCells);
     L.gh_tiles_y = (int)div_up(L.ch, kGhSegRows);
     L.gh_begin = gh;
@@ -275,6 +281,8 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
     anchors_pf += (long long)L.sw * L.sh;
   }
   H.gh_total = gh;
+  H.gr_total = gr;
+  H.fld_total = fld;
   H.sc_total = sc;
   H.cell_total = cells;
   H.cells_per_frame = n ? cells / n : 0;
@@ -285,6 +293,8 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
 
   TRY(P.desc.ensure(sizeof(PlanDesc)));
   TRY(P.arena.ensure(sizeof(double) * std::max<long long>(1, P.arena_elems)));
+  TRY(P.fmag.ensure(sizeof(double) * std::max<long long>(1, fld)));
+  TRY(P.fori.ensure(std::max<long long>(1, fld)));
   TRY(P.bins.ensure(sizeof(double) * kBins * std::max<long long>(1, cells)));
   TRY(P.energy.ensure(sizeof(double) * std::max<long long>(1, cells)));
   TRY(P.feat64.ensure(sizeof(double) * kFeat * std::max<long long>(1, cells)));
@@ -353,13 +363,13 @@ int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long lon
   CK(cudaMemsetAsync(P.overflow.p, 0, sizeof(int), c->st));
   if (ns > 0) {
     int s1 = 0;
-    if (P.scored[0] == 0) {
-      launch_gradhist_levels(L, P.host, Pd, 0, 1, in, pix == BL_PIX_U8 ? 0 : 1, P.bins.as<double>(),
-                             P.energy.as<double>());
+    if (P.scored[0] == 0) {  // level 0 reads the caller's frames (u8 or f64)
+      launch_grad(L, P.host, Pd, 0, 1, in, pix == BL_PIX_U8 ? 0 : 1, P.fmag.as<double>(), P.fori.as<uint8_t>());
       s1 = 1;
     }
-    launch_gradhist_levels(L, P.host, Pd, s1, ns, P.arena.as<double>(), 1, P.bins.as<double>(),
-                           P.energy.as<double>());
+    launch_grad(L, P.host, Pd, s1, ns, P.arena.as<double>(), 1, P.fmag.as<double>(), P.fori.as<uint8_t>());
+    launch_gradhist(L, P.host, Pd, P.fmag.as<double>(), P.fori.as<uint8_t>(), P.bins.as<double>(),
+                    P.energy.as<double>());
   }
   stage_mark(c, BL_STAGE_FEATURES);
   launch_features(L, P.host, Pd, P.bins.as<double>(), P.energy.as<double>(), P.feat64.as<double>(),
@@ -564,6 +574,10 @@ void single_level_plan(PlanDesc& H, int w, int h, int cw, int ch) {
   L.sh = ch - 9;
   L.pix_pitch = w;
   L.pix_fstride = (long long)w * h;
+  L.gr_tiles_x = (int)div_up(w, 32);
+  L.gr_tiles_y = (int)div_up(h, 32);
+  H.gr_total = (long long)L.gr_tiles_x * L.gr_tiles_y;
+  H.fld_total = (long long)w * h;
   L.gh_tiles_x = (int)div_up(cw, kGhCells);
   L.gh_tiles_y = (int)div_up(ch, kGhSegRows);
   H.gh_total = (long long)L.gh_tiles_x * L.gh_tiles_y;
@@ -911,7 +925,11 @@ int bl_compute_gradients(bl_ctx* c, const double* image, int w, int h, uint8_t* 
   TRY(to_device(c, c->s_a, image, sizeof(double) * w * h, &src));
   TRY(c->s_b.ensure(sizeof(double) * w * h));
   TRY(c->s_c.ensure((size_t)w * h));
-  launch_gradients(launch_of(c), (const double*)src, w, h, c->s_c.as<uint8_t>(), c->s_b.as<double>());
+  PlanDesc H;
+  single_level_plan(H, w, h, w / 8, h / 8);
+  TRY(c->s_desc.ensure(sizeof(PlanDesc)));
+  CK(cudaMemcpyAsync(c->s_desc.p, &H, sizeof H, cudaMemcpyHostToDevice, c->st));
+  launch_grad(launch_of(c), H, c->s_desc.as<PlanDesc>(), 0, 1, src, 1, c->s_b.as<double>(), c->s_c.as<uint8_t>());
   CK(cudaMemcpyAsync(ori, c->s_c.p, (size_t)w * h, cudaMemcpyDefault, c->st));
   return from_device(c, mag, c->s_b.p, sizeof(double) * w * h);
 }
@@ -931,8 +949,8 @@ int bl_histogramize(bl_ctx* c, const uint8_t* ori, const double* mag, int w, int
   TRY(c->s_desc.ensure(sizeof(PlanDesc)));
   CK(cudaMemcpyAsync(c->s_desc.p, &H, sizeof H, cudaMemcpyHostToDevice, c->st));
   TRY(c->s_b.ensure(sizeof(double) * kBins * cw * ch));
-  launch_gradhist_field(launch_of(c), H, c->s_desc.as<PlanDesc>(), (const uint8_t*)o, (const double*)m,
-                        c->s_b.as<double>());
+  launch_gradhist(launch_of(c), H, c->s_desc.as<PlanDesc>(), (const double*)m, (const uint8_t*)o,
+                  c->s_b.as<double>(), nullptr);
   return from_device(c, bins, c->s_b.p, sizeof(double) * kBins * cw * ch);
 }
 
@@ -988,8 +1006,12 @@ int bl_extract_features(bl_ctx* c, const double* image, int w, int h, double* fe
   TRY(c->s_b.ensure(sizeof(double) * kBins * cells));
   TRY(c->s_c.ensure(sizeof(double) * cells));
   TRY(c->s_d.ensure(sizeof(double) * kFeat * cells));
+  TRY(c->s_e.ensure(sizeof(double) * w * h + (size_t)w * h + 16));
+  double* fm = c->s_e.as<double>();
+  uint8_t* fo = reinterpret_cast<uint8_t*>(fm + (size_t)w * h);
   const Launch L = launch_of(c);
-  launch_gradhist_levels(L, H, c->s_desc.as<PlanDesc>(), 0, 1, src, 1, c->s_b.as<double>(), c->s_c.as<double>());
+  launch_grad(L, H, c->s_desc.as<PlanDesc>(), 0, 1, src, 1, fm, fo);
+  launch_gradhist(L, H, c->s_desc.as<PlanDesc>(), fm, fo, c->s_b.as<double>(), c->s_c.as<double>());
   launch_features(L, H, c->s_desc.as<PlanDesc>(), c->s_b.as<double>(), c->s_c.as<double>(), c->s_d.as<double>(),
                   nullptr);
   if (bins) CK(cudaMemcpyAsync(bins, c->s_b.p, sizeof(double) * kBins * cells, cudaMemcpyDefault, c->st));
@@ -1048,6 +1070,20 @@ int bl_orientation_bins(bl_ctx* c, const double* gx, const double* gy, int64_t n
   TRY(c->s_c.ensure((size_t)n));
   launch_orientation(launch_of(c), (const double*)a, (const double*)b, n, c->s_c.as<uint8_t>());
   return from_device(c, bins, c->s_c.p, (size_t)n);
+}
+
+int bl_debug_sqrt(bl_ctx* c, const double* in, int64_t n, double* fast, double* ieee) {
+  if (!c || !in || !fast || !ieee) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (n <= 0) return BL_OK;
+  TRY(use_device(c));
+  const void* a = nullptr;
+  TRY(to_device(c, c->s_a, in, sizeof(double) * n, &a));
+  TRY(c->s_b.ensure(sizeof(double) * n));
+  TRY(c->s_c.ensure(sizeof(double) * n));
+  launch_sqrt_check(launch_of(c), (const double*)a, n, c->s_b.as<double>(), c->s_c.as<double>());
+  CK(cudaMemcpyAsync(fast, c->s_b.p, sizeof(double) * n, cudaMemcpyDefault, c->st));
+  return from_device(c, ieee, c->s_c.p, sizeof(double) * n);
 }
 
 }  // extern "C"

@@ -48,7 +48,10 @@ struct LevelDesc {
   long long f32_off;     // fp32 planar features: float offset of frame 0
   int cw_pad, ch_pad;    // fp32 planar plane dims
   long long f32_fstride; // floats between frames (= 32 * ch_pad * cw_pad)
+  long long fld_off;     // gradient field (f64 magnitude / u8 bin planes): offset of frame 0
   // work decomposition (block ranges are global across levels)
+  int gr_tiles_x, gr_tiles_y;  // gradient 32x32-pixel blocks per frame
+  long long gr_begin;          // first gradient block id of this level
   int gh_tiles_x, gh_tiles_y;  // gradHist warp tiles per frame
   long long gh_begin;          // first gradHist warp-tile id of this level
   int sc_tiles_x, sc_tiles_y;  // screening warp tiles per frame
@@ -61,6 +64,8 @@ struct PlanDesc {
   int n_frames;
   int n_scored;                // scored levels (eligible and >= one window)
   LevelDesc lv[kMaxLevels];
+  long long gr_total;          // total gradient blocks
+  long long fld_total;         // gradient-field pixels over levels and frames
   long long gh_total;          // total gradHist warp tiles
   long long sc_total;          // total screening warp tiles
   long long cell_total;        // total cells over levels and frames
@@ -116,13 +121,12 @@ void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int s
                      long long s_fstride, double* dst, int dw, int dh, long long d_fstride, int n);
 // bl_hog.cu
 void set_direction_table(const double* ux, const double* uy);
-void launch_gradhist_levels(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, int s_lo,
-                            int s_hi, const void* base, int src_kind /*0 u8, 1 f64*/, double* bins,
-                            double* energy);
-void launch_gradhist_field(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd,
-                           const uint8_t* ori, const double* mag, double* bins);
-void launch_gradients(const Launch& L, const double* img, int w, int h, uint8_t* ori, double* mag);
+void launch_grad(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, int s_lo, int s_hi, const void* base,
+                 int src_kind /*0 u8, 1 f64*/, double* fmag, uint8_t* fori);
+void launch_gradhist(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, const double* fmag,
+                     const uint8_t* fori, double* bins, double* energy);
 void launch_orientation(const Launch& L, const double* gx, const double* gy, long long n, uint8_t* out);
+void launch_sqrt_check(const Launch& L, const double* in, long long n, double* fast, double* ieee);
 void launch_energy(const Launch& L, const double* bins, long long cells, double* energy);
 void launch_features(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, const double* bins,
                      const double* energy, double* feat64, float* feat32);

@@ -96,6 +96,31 @@ def test_orientation_exhaustive_integer_gradients(ctx, oracle):
     assert list(ctx.orientation_bins([0.0, 0.0, 0.0], [10.0, -10.0, 0.0])) == [4, 14, 0]
 
 
+def test_sqrt_fast_matches_ieee(ctx):
+    """The branch-free gradient-magnitude sqrt equals IEEE sqrt on its whole input range."""
+    r = rng(13)
+    xs = [np.exp(r.uniform(np.log(1e-300), np.log(1e300), 4_000_000)),
+          r.uniform(0, 2 * 255.0 ** 2, 4_000_000),                 # the u8 / level-pixel range
+          np.arange(1, 2 * 255 ** 2 + 1, dtype=np.float64),          # every integer gradient norm^2
+          np.nextafter(np.arange(1, 200001, dtype=np.float64) ** 2, 0),  # just below perfect squares
+          np.nextafter(np.arange(1, 200001, dtype=np.float64) ** 2, np.inf)]
+    for x in xs:
+        fast, ieee = ctx.debug_sqrt(x)
+        assert np.array_equal(fast, ieee)
+        assert np.array_equal(ieee, np.sqrt(x))
+
+
+def test_orientation_pathological_magnitudes(ctx, oracle):
+    """Gradients far outside fp32 range take the exact slow path inside the batched kernel."""
+    img = np.full((48, 48), 1e-310)
+    img[::3, ::2] = 0.0
+    img[10:20, 10:20] = 3e-200
+    img[30:40, 5:15] = 255.0
+    f, b, e = ctx.extract_features(img, want_cells=True)
+    assert np.array_equal(b, oracle.histogramize(*oracle.compute_gradients(img)))
+    assert np.array_equal(f, oracle.extract_features(img))
+
+
 def test_gradients_basic_cases(ctx):
     ori, mag = ctx.compute_gradients(np.full((10, 10), 42.0))
     assert np.all(mag == 0)
