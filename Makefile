@@ -25,7 +25,7 @@ FAST_CU  := bl_classify bl_capi
 OBJS     := $(addprefix $(BUILD)/,$(addsuffix .o,$(EXACT_CU) $(FAST_CU)))
 HDRS     := $(CSRC)/bl_internal.cuh include/blinkline_b200.h
 
-all: $(LIB) $(CPPLIB) oracle
+all: $(LIB) $(CPPLIB) tests/cpp/test_dropin oracle
 
 $(BUILD):
 	@mkdir -p $(BUILD)
@@ -43,6 +43,10 @@ $(CPPLIB): $(PKG)/cpp/blinkline_gpu.cpp $(PKG)/cpp/blinkline_gpu.hpp include/bli
 	$(CXX) -std=c++20 -O2 -fPIC -shared -I$(PKG)/cpp -Iinclude -o $@ $(PKG)/cpp/blinkline_gpu.cpp \
 	  -L$(PKG) -lblinkline_b200 -Wl,-rpath,'$$ORIGIN'
 
+tests/cpp/test_dropin: tests/cpp/test_dropin.cpp $(CPPLIB)
+	$(CXX) -std=c++20 -O2 -I$(PKG)/cpp -o $@ $< -L$(PKG) -lblinkline_gpu -lblinkline_b200 \
+	  -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
 oracle:
 	$(MAKE) -s -C oracle
 
@@ -50,6 +54,6 @@ ref:
 	$(MAKE) -s -C oracle ref
 
 clean:
-	rm -rf $(BUILD) $(LIB) $(CPPLIB)
+	rm -rf $(BUILD) $(LIB) $(CPPLIB) tests/cpp/test_dropin
 
 .PHONY: all oracle ref clean

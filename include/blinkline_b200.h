@@ -76,6 +76,13 @@ enum {
 
 /* ------------------------------------------------------------------ context ---- */
 int bl_abi_version(void);
+/* Host-only geometry of a detect batch, no device work: pyramid level dims (image.cpp:158-172),
+ * the scored levels -- eligible_scales (detector.cpp:144-155) with room for a window
+ * (detector.cpp:163-167) -- and per scored level the scale (5/6)^k and the box side
+ * round_half_up(window_px / c) (detector.cpp:104-105). */
+int bl_plan_geometry(int w, int h, int window_cells, int cell_px, int scale_num, int scale_den,
+                     double min_face_ratio, int* dims, int* scored, double* scale_c, int* side,
+                     int max_levels, int* n_levels, int* n_scored);
 const char* bl_last_error(void);
 int bl_device_count(int* n);
 int bl_ctx_create(int device, bl_ctx** out);

@@ -68,6 +68,8 @@ _vp, _i32, _i64, _u64, _dbl, _sz = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64,
 _P = C.POINTER
 _SIGS = {
     "bl_abi_version": (C.c_int, []),
+    "bl_plan_geometry": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dbl, _vp, _vp, _vp, _vp,
+                                   C.c_int, _P(C.c_int), _P(C.c_int)]),
     "bl_last_error": (C.c_char_p, []),
     "bl_device_count": (C.c_int, [_P(C.c_int)]),
     "bl_ctx_create": (C.c_int, [C.c_int, _P(_vp)]),
@@ -370,6 +372,21 @@ class Context:
         out = np.zeros(len(gx), np.uint8)
         _err(lib.bl_orientation_bins(self._h, gx.ctypes.data, gy.ctypes.data, len(gx), out.ctypes.data))
         return out
+
+
+def plan_geometry(w, h, window_cells=10, cell_px=8, scale_num=5, scale_den=6, min_face_ratio=0.2):
+    """Host-only batch geometry: (level dims [(w,h)...], scored levels, scale per scored level,
+    box side per scored level).  No GPU needed."""
+    dims = np.zeros(128, np.int32)
+    scored = np.zeros(64, np.int32)
+    sc = np.zeros(64)
+    side = np.zeros(64, np.int32)
+    nl, ns = C.c_int(0), C.c_int(0)
+    _err(lib.bl_plan_geometry(w, h, window_cells, cell_px, scale_num, scale_den, float(min_face_ratio),
+                              dims.ctypes.data, scored.ctypes.data, sc.ctypes.data, side.ctypes.data, 64,
+                              C.byref(nl), C.byref(ns)))
+    levels = [(int(dims[2 * k]), int(dims[2 * k + 1])) for k in range(nl.value)]
+    return levels, [int(v) for v in scored[:ns.value]], sc[:ns.value].copy(), [int(v) for v in side[:ns.value]]
 
 
 # ------------------------------------------------ reference-named module functions

@@ -266,7 +266,7 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
     L.fld_off = fld;
     fld += (long long)n * L.w * L.h;
     L.gr_tiles_x = (int)div_up(L.w, 32);
-    L.gr_tiles_y = (int)div_up(L.h, 32);
+    L.gr_tiles_y = (int)div_up(L.h, 64);
     L.gr_begin = gr;
     gr += (long long)n * L.gr_tiles_x * L.gr_tiles_y;
     L.gh_tiles_x = (int)div_up(L.cw, kGhCells);
@@ -575,7 +575,7 @@ void single_level_plan(PlanDesc& H, int w, int h, int cw, int ch) {
   L.pix_pitch = w;
   L.pix_fstride = (long long)w * h;
   L.gr_tiles_x = (int)div_up(w, 32);
-  L.gr_tiles_y = (int)div_up(h, 32);
+  L.gr_tiles_y = (int)div_up(h, 64);
   H.gr_total = (long long)L.gr_tiles_x * L.gr_tiles_y;
   H.fld_total = (long long)w * h;
   L.gh_tiles_x = (int)div_up(cw, kGhCells);
@@ -591,6 +591,39 @@ void single_level_plan(PlanDesc& H, int w, int h, int cw, int ch) {
 extern "C" {
 
 int bl_abi_version(void) { return BL_ABI_VERSION; }
+
+int bl_plan_geometry(int w, int h, int window_cells, int cell_px, int scale_num, int scale_den,
+                     double min_face_ratio, int* dims, int* scored, double* scale_c, int* side, int max_levels,
+                     int* n_levels, int* n_scored) {
+  if (!n_levels || !n_scored) return set_err(BL_ERR_INVALID, "null out");
+  if (w < 1 || h < 1) return set_err(BL_ERR_INVALID, "make_image: dimensions must be >= 1");
+  if (window_cells != kWin) return set_err(BL_ERR_INVALID, "filter must carry exactly 3100 weights");
+  if (cell_px < 1 || scale_num < 1 || scale_den < 1) return set_err(BL_ERR_MODEL, "bad detector geometry");
+  std::vector<int> lw, lh;
+  const int window = window_cells * cell_px;
+  pyramid_dims(w, h, window, lw, lh);
+  *n_levels = (int)lw.size();
+  const double min_face = min_face_ratio * std::min(w, h);
+  int ns = 0;
+  for (int k = 0; k < (int)lw.size(); ++k) {
+    if (k < max_levels && dims) {
+      dims[2 * k] = lw[k];
+      dims[2 * k + 1] = lh[k];
+    }
+    const double c = std::pow(double(scale_num) / scale_den, double(k));
+    const double detectable = window / c;
+    if (!(detectable >= min_face * (1.0 - 1e-9))) continue;
+    if (lw[k] / cell_px < window_cells || lh[k] / cell_px < window_cells) continue;
+    if (ns < max_levels) {
+      if (scored) scored[ns] = k;
+      if (scale_c) scale_c[ns] = c;
+      if (side) side[ns] = round_half_up_host(window / c);
+    }
+    ++ns;
+  }
+  *n_scored = ns;
+  return BL_OK;
+}
 
 const char* bl_last_error(void) { return g_err.c_str(); }
 

@@ -25,7 +25,7 @@ constexpr int kScreenSmem = kWin * kFeat * kWBlock * (int)sizeof(float);  // 64,
 
 constexpr int kScreenWarps = 8;  // warps per CTA sharing one smem copy of the weights
 
-__global__ void __launch_bounds__(kScreenWarps * 32, 2) k_screen(const PlanDesc* __restrict__ P,
+__global__ void __launch_bounds__(kScreenWarps * 32, 2) k_screen(const PlanDesc* __restrict__ P, const LevelBegins B,
                                                 const float* __restrict__ feat32,
                                                 const float* __restrict__ w32,
                                                 const float* __restrict__ cut,
@@ -41,8 +41,7 @@ __global__ void __launch_bounds__(kScreenWarps * 32, 2) k_screen(const PlanDesc*
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long wid = (long long)blockIdx.x * kScreenWarps + warp;
   if (wid >= total) return;
-  int s = 0;
-  while (s + 1 < P->n_scored && wid >= P->lv[s + 1].sc_begin) ++s;
+  const int s = find_level(B, wid);
   const LevelDesc& D = P->lv[s];
   const long long local = wid - D.sc_begin;
   const int tiles = D.sc_tiles_x * D.sc_tiles_y;
@@ -160,7 +159,11 @@ void launch_screen(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, cons
     cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, kScreenSmem);
     attr = true;
   }
-  k_screen<<<(unsigned)div_up(Ph.sc_total, kScreenWarps), kScreenWarps * 32, kScreenSmem, L.st>>>(Pd, feat32, w32, cut, cand,
+  LevelBegins B{};
+  B.n = Ph.n_scored;
+  for (int s = 0; s < Ph.n_scored; ++s) B.b[s] = Ph.lv[s].sc_begin;
+  B.b[B.n] = Ph.sc_total;
+  k_screen<<<(unsigned)div_up(Ph.sc_total, kScreenWarps), kScreenWarps * 32, kScreenSmem, L.st>>>(Pd, B, feat32, w32, cut, cand,
                                                                         n_cand, cand_cap, Ph.sc_total);
   ++*L.counter;
 }

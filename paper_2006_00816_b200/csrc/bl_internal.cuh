@@ -13,6 +13,8 @@
 
 #include "../../include/blinkline_b200.h"
 
+#define BL_HD_INLINE __host__ __device__ __forceinline__
+
 namespace blb {
 
 constexpr int kBins = 18;
@@ -71,6 +73,20 @@ struct PlanDesc {
   long long cell_total;        // total cells over levels and frames
   long long cells_per_frame;
 };
+
+// Per-launch table of the first work-item id of each scored level, passed BY VALUE so the
+// level search reads the kernel-parameter constant bank instead of global memory.
+struct LevelBegins {
+  int n;
+  long long b[kMaxLevels + 1];  // b[s] = first id of level s; b[n] = total
+};
+
+BL_HD_INLINE int find_level(const LevelBegins& B, long long id) {
+  int s = 0;
+#pragma unroll 1
+  while (s + 1 < B.n && id >= B.b[s + 1]) ++s;
+  return s;
+}
 
 // Candidate from the fp32 screen: (frame, scored-level slot, filter, cx, cy).
 struct Candidate {
