@@ -176,12 +176,10 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
+    from paper_2006_00816_b200.sharding import max_over_ranks as _mor
+
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return _mor(x, device=torch.device("cuda", local))
 
     # ---- device-resident timed region
     for _ in range(args.warmup):
@@ -307,10 +305,17 @@ def cpu_baseline(frames, det, ert, n):
     sample = np.ascontiguousarray(frames[:n])
     ref.run_batch_u8(sample[:threads], det, ert, threads)  # warm-up (page-in, model build)
     t0 = time.perf_counter()
-    faces, counts, _ = ref.run_batch_u8(sample, det, ert, threads)
-    dt = time.perf_counter() - t0
-    return {"value": round(n / dt, 3), "unit": "frames/s", "cores": threads, "kind": kind,
-            "sample": f"{n} frames {W}x{H}, {faces} faces landmarked, {dt:.1f} s wall on {threads} threads"}
+    reps, faces = 0, 0
+    while True:  # ~10-30 s of CPU work: repeat the sample until >= 10 s wall
+        f, counts, _ = ref.run_batch_u8(sample, det, ert, threads)
+        faces += f
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt >= 10.0 or reps >= 200:
+            break
+    return {"value": round(n * reps / dt, 3), "unit": "frames/s", "cores": threads, "kind": kind,
+            "sample": f"{n} distinct {W}x{H} frames x {reps} passes = {n * reps} frames, {faces} faces "
+                      f"landmarked, {dt:.1f} s wall on {threads} threads"}
 
 
 # ------------------------------------------------------------------ reference arm
