@@ -152,7 +152,7 @@ struct bl_ctx {
   ErtState ert;
   Plan plan;
   // ERT working set
-  DevBuf ert_cur, ert_out, ert_leaf, ert_boxes, ert_frames, ert_nfaces, ert_err, ert_input;
+  DevBuf ert_cur, ert_out, ert_leaf, ert_leafs, ert_tf, ert_boxes, ert_frames, ert_nfaces, ert_err, ert_input;
   // scratch for stage functions
   DevBuf s_a, s_b, s_c, s_d, s_e, s_desc;
   // pinned host staging for counts
@@ -445,13 +445,22 @@ int run_ert(bl_ctx* c, const void* frames, int pix, int w, int h, long long pitc
   const int L2 = 2 * E.dev.L;
   TRY(c->ert_cur.ensure(sizeof(double) * L2 * std::max(1, nf)));
   TRY(c->ert_out.ensure(sizeof(double) * L2 * std::max(1, nf)));
+  TRY(c->ert_tf.ensure(sizeof(double2) * std::max(1, nf)));
   TRY(c->ert_err.ensure(sizeof(int)));
+  // leaf indices: the caller's [face][T*K] buffer, else a per-level scratch [face][K]
+  long long leaf_stride = (long long)E.dev.T * E.dev.K;
+  uint8_t* leaf = leaf_dev;
+  if (!leaf) {
+    TRY(c->ert_leafs.ensure((size_t)std::max(1, nf) * E.dev.K + 16));
+    leaf = c->ert_leafs.as<uint8_t>();
+    leaf_stride = E.dev.K;
+  }
   CK(cudaMemsetAsync(c->ert_err.p, 0, sizeof(int), c->st));
   launch_ert_init(L, E.dev, n_faces_dev, nf, c->ert_cur.as<double>());
-  const int blocks = std::max(1, std::min(nf, 148 * 8));
   for (int t = 0; t < E.dev.T; ++t)
     launch_ert_level(L, E.dev, t, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
-                     n_faces_dev, nf, c->ert_cur.as<double>(), leaf_dev, c->ert_err.as<int>(), blocks);
+                     n_faces_dev, nf, c->ert_cur.as<double>(), c->ert_tf.as<double2>(),
+                     leaf_dev ? leaf + (long long)t * E.dev.K : leaf, leaf_stride, c->ert_err.as<int>());
   launch_ert_finish(L, E.dev, boxes, box_stride, n_faces_dev, nf, c->ert_cur.as<double>(),
                     c->ert_out.as<double>());
   return BL_OK;

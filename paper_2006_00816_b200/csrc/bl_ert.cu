@@ -1,20 +1,20 @@
 // Ensemble-of-regression-trees 68-landmark cascade (ert.cpp:15-136) on the device.
 //
-// One launch per cascade level t (the levels are strictly sequential, ert.cpp:108); inside
-// a launch every face of the batch is independent.  A CTA handles one face at a time:
-//   1. similarity transform current -> mean (ert.cpp:26-69): the sums run sequentially in
-//      the reference's order on one thread (bit-identical), then CUDA's hypot/atan2/cos/sin
-//      (<= 2 ulp from glibc: the only non-bit-exact step of the whole path);
-//   2. one thread per tree walks its F splits (level order, left iff Ia - Ib > thr,
-//      ert.cpp:87-97), sampling the ORIGINAL frame through apply_linear + box map +
-//      llround + clamp (ert.cpp:20-24, 71-85);
-//   3. one thread per coordinate sums the K selected leaf rows IN TREE ORDER in fp64
-//      (ert.cpp:118-121) and applies cur += shrinkage * delta (ert.cpp:123-126).
+// The cascade levels are strictly sequential (ert.cpp:108); within a level every face and
+// every tree is independent.  Per level three fully parallel kernels:
+//   1. k_ert_xform    thread per face: similarity transform current -> mean (ert.cpp:26-69),
+//                     sums sequential in the reference's order (bit-identical), then CUDA's
+//                     hypot/atan2/cos/sin (<= 2 ulp from glibc: the only non-bit-exact step);
+//   2. k_ert_traverse thread per (face, tree): walks the F splits in level order, left iff
+//                     Ia - Ib > thr (ert.cpp:87-97), sampling the ORIGINAL frame through
+//                     apply_linear + box map + llround + clamp (ert.cpp:20-24, 71-85);
+//   3. k_ert_accum    thread per (face, coordinate): sums the K selected leaf rows IN TREE
+//                     ORDER in fp64 (ert.cpp:118-121), cur += shrinkage * delta (:123-126).
 // Compiled with --fmad=false; all arithmetic mirrors the reference operation for operation.
 //
-// Per-level launches keep one level's trees (K * 2^F * L * 16 B = 8.7 MB at 500 trees,
-// depth 4, L = 68) hot in L2 for every face of the batch: HBM reads the model once per
-// batch, L2 serves the 1088-B leaf row each (face, tree) selects.
+// Level-synchronous launches keep one level's trees (K * 2^F * L * 16 B = 8.7 MB at 500
+// trees, depth 4, L = 68) resident in L2 for every face of the batch: HBM reads the model
+// once per batch; L2 serves the 1088-B leaf row each (face, tree) selects.
 #include "bl_internal.cuh"
 
 namespace blb {
@@ -50,107 +50,127 @@ BL_DEV double sample_px(const void* fr, int w, int h, long long pitch, int bx, i
   return __ldg((const double*)fr + (long long)iy * pitch + ix);
 }
 
-template <bool U8>
-__global__ void __launch_bounds__(256) k_ert_level(ErtDev M, int t, const void* __restrict__ frames,
-                                                   int w, int h, long long pitch, long long fstride,
-                                                   const int* __restrict__ face_frame,
-                                                   const int* __restrict__ boxes, int box_stride,
-                                                   const int* __restrict__ n_faces, int cap,
-                                                   double* __restrict__ cur_g,
-                                                   uint8_t* __restrict__ leaf_out,
+// (1) similarity_transform(current, mean) per face, ert.cpp:26-69: sequential sums in the
+// reference's order (bit-identical), then CUDA hypot/atan2/cos/sin.  Stores the linear part
+// (scale*cos, scale*sin) that apply_linear recomputes for every sample (ert.cpp:21-22).
+__global__ void __launch_bounds__(128) k_ert_xform(ErtDev M, const int* __restrict__ n_faces, int cap,
+                                                   const double* __restrict__ cur_g, double2* __restrict__ tf,
                                                    int* __restrict__ err) {
-  extern __shared__ double ert_smem[];
-  const int L2 = 2 * M.L;
-  double* s_cur = ert_smem;                                  // L2 doubles
-  double* s_tf = ert_smem + L2;                              // A, B
-  uint8_t* s_leaf = reinterpret_cast<uint8_t*>(ert_smem + L2 + 2);  // K bytes
   const int n = min(*n_faces, cap);
-  const int K = M.K, S = M.S, NL = M.NL;
-  for (int face = blockIdx.x; face < n; face += gridDim.x) {
-    double* cur = cur_g + (long long)face * L2;
-    for (int i = threadIdx.x; i < L2; i += blockDim.x) s_cur[i] = cur[i];
-    __syncthreads();
-    if (threadIdx.x == 0) {  // similarity_transform(current, mean), ert.cpp:26-69
-      double mfx = 0.0, mfy = 0.0;
-      for (int i = 0; i < M.L; ++i) {
-        mfx = dadd(mfx, s_cur[2 * i]);
-        mfy = dadd(mfy, s_cur[2 * i + 1]);
-      }
-      mfx = ddiv(mfx, (double)M.L);
-      mfy = ddiv(mfy, (double)M.L);
-      double sff = 0.0, sre = 0.0, sim = 0.0;
-      for (int i = 0; i < M.L; ++i) {
-        const double fx = dsub(s_cur[2 * i], mfx);
-        const double fy = dsub(s_cur[2 * i + 1], mfy);
-        const double txp = dsub(M.mean_xy[2 * i], M.mean_cx);
-        const double typ = dsub(M.mean_xy[2 * i + 1], M.mean_cy);
-        sff = dadd(sff, dadd(dmul(fx, fx), dmul(fy, fy)));
-        sre = dadd(sre, dadd(dmul(fx, txp), dmul(fy, typ)));
-        sim = dadd(sim, dsub(dmul(fx, typ), dmul(fy, txp)));
-      }
-      double A = 0.0, B = 0.0;
-      if (!(sff > 0.0)) {
-        atomicExch(err, 1);  // "source shape has no spread" (ert.cpp:56-57)
-      } else {
-        const double a = ddiv(sre, sff), b = ddiv(sim, sff);
-        const double scale = hypot(a, b);
-        if (!(scale > 0.0)) {
-          atomicExch(err, 2);  // "target shape has no spread" (ert.cpp:62-63)
-        } else {
-          const double rot = atan2(b, a);
-          A = dmul(scale, cos(rot));  // apply_linear recomputes these per sample (ert.cpp:21-22);
-          B = dmul(scale, sin(rot));  // the values are the same every time
-        }
-      }
-      s_tf[0] = A;
-      s_tf[1] = B;
-    }
-    __syncthreads();
-    const double A = s_tf[0], B = s_tf[1];
-    const int* bx = boxes + (long long)face * box_stride;
-    const int X = bx[0], Y = bx[1], W = bx[2], H = bx[3];
-    const void* fr = (const char*)frames + (long long)face_frame[face] * fstride * (U8 ? 1 : 8);
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
-      const long long tree = (long long)t * K + k;
-      int node = 0;
-      while (node < S) {  // traverse_tree, ert.cpp:87-97
-        const long long sn = tree * S + node;
-        const short2 an = *reinterpret_cast<const short2*>(M.anchors + 2 * sn);
-        const double* sp = M.split + 5 * sn;
-        const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, s_cur, A, B, an.x, __ldg(sp), __ldg(sp + 1));
-        const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, s_cur, A, B, an.y, __ldg(sp + 2), __ldg(sp + 3));
-        node = dsub(ia, ib) > __ldg(sp + 4) ? 2 * node + 1 : 2 * node + 2;
-      }
-      const int leaf = node - S;
-      s_leaf[k] = (uint8_t)leaf;
-      if (leaf_out) leaf_out[((long long)face * M.T + t) * K + k] = (uint8_t)leaf;
-    }
-    __syncthreads();
-    for (int c = threadIdx.x; c < L2; c += blockDim.x) {
-      const double* lv = M.leaves + (long long)t * K * NL * L2 + c;
-      double acc = 0.0;
-#pragma unroll 4
-      for (int k = 0; k < K; ++k) acc = dadd(acc, __ldg(lv + ((long long)k * NL + s_leaf[k]) * L2));
-      cur[c] = dadd(s_cur[c], dmul(M.shrinkage, acc));  // ert.cpp:123-126
-    }
-    __syncthreads();
+  const int face = blockIdx.x * blockDim.x + threadIdx.x;
+  if (face >= n) return;
+  const double* cur = cur_g + (long long)face * 2 * M.L;
+  double mfx = 0.0, mfy = 0.0;
+  for (int i = 0; i < M.L; ++i) {
+    mfx = dadd(mfx, cur[2 * i]);
+    mfy = dadd(mfy, cur[2 * i + 1]);
   }
+  mfx = ddiv(mfx, (double)M.L);
+  mfy = ddiv(mfy, (double)M.L);
+  double sff = 0.0, sre = 0.0, sim = 0.0;
+  for (int i = 0; i < M.L; ++i) {
+    const double fx = dsub(cur[2 * i], mfx);
+    const double fy = dsub(cur[2 * i + 1], mfy);
+    const double txp = dsub(__ldg(M.mean_xy + 2 * i), M.mean_cx);
+    const double typ = dsub(__ldg(M.mean_xy + 2 * i + 1), M.mean_cy);
+    sff = dadd(sff, dadd(dmul(fx, fx), dmul(fy, fy)));
+    sre = dadd(sre, dadd(dmul(fx, txp), dmul(fy, typ)));
+    sim = dadd(sim, dsub(dmul(fx, typ), dmul(fy, txp)));
+  }
+  double A = 0.0, B = 0.0;
+  if (!(sff > 0.0)) {
+    atomicExch(err, 1);  // "source shape has no spread" (ert.cpp:56-57)
+  } else {
+    const double a = ddiv(sre, sff), b = ddiv(sim, sff);
+    const double scale = hypot(a, b);
+    if (!(scale > 0.0)) {
+      atomicExch(err, 2);  // "target shape has no spread" (ert.cpp:62-63)
+    } else {
+      const double rot = atan2(b, a);
+      A = dmul(scale, cos(rot));
+      B = dmul(scale, sin(rot));
+    }
+  }
+  tf[face] = make_double2(A, B);
 }
 
-size_t ert_smem_bytes(const ErtDev& M) { return sizeof(double) * (2 * M.L + 2) + M.K + 16; }
+// (2) one thread per (face, tree): traverse_tree (ert.cpp:87-97) with sample_intensity
+// (ert.cpp:71-85) on the ORIGINAL frame; writes the leaf index.
+template <bool U8>
+__global__ void __launch_bounds__(256) k_ert_traverse(ErtDev M, int t, const void* __restrict__ frames, int w,
+                                                      int h, long long pitch, long long fstride,
+                                                      const int* __restrict__ face_frame,
+                                                      const int* __restrict__ boxes, int box_stride,
+                                                      const int* __restrict__ n_faces, int cap,
+                                                      const double* __restrict__ cur_g,
+                                                      const double2* __restrict__ tf,
+                                                      uint8_t* __restrict__ leaf_idx, long long leaf_stride) {
+  const int n = min(*n_faces, cap);
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int K = M.K, S = M.S;
+  if (g >= (long long)n * K) return;
+  const int face = (int)(g / K), k = (int)(g - (long long)face * K);
+  const double2 ab = tf[face];
+  const double* cur = cur_g + (long long)face * 2 * M.L;
+  const int* bx = boxes + (long long)face * box_stride;
+  const int X = bx[0], Y = bx[1], W = bx[2], H = bx[3];
+  const void* fr = (const char*)frames + (long long)face_frame[face] * fstride * (U8 ? 1 : 8);
+  const long long tree = (long long)t * K + k;
+  int node = 0;
+  while (node < S) {
+    const long long sn = tree * S + node;
+    const short2 an = *reinterpret_cast<const short2*>(M.anchors + 2 * sn);
+    const double* sp = M.split + 5 * sn;
+    const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, cur, ab.x, ab.y, an.x, __ldg(sp), __ldg(sp + 1));
+    const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, cur, ab.x, ab.y, an.y, __ldg(sp + 2), __ldg(sp + 3));
+    node = dsub(ia, ib) > __ldg(sp + 4) ? 2 * node + 1 : 2 * node + 2;
+  }
+  leaf_idx[(long long)face * leaf_stride + k] = (uint8_t)(node - S);
+}
+
+// (3) one thread per (face, coordinate): sum the K selected leaf rows IN TREE ORDER in fp64
+// (ert.cpp:118-121), then cur += shrinkage * delta (ert.cpp:123-126).  Consecutive threads
+// read consecutive coordinates of one leaf row (coalesced, L2-resident for the level); the
+// loads of 16 trees are issued ahead of their adds.
+__global__ void __launch_bounds__(256) k_ert_accum(ErtDev M, int t, const int* __restrict__ n_faces, int cap,
+                                                   double* __restrict__ cur_g,
+                                                   const uint8_t* __restrict__ leaf_idx, long long leaf_stride) {
+  const int n = min(*n_faces, cap);
+  const int L2 = 2 * M.L, K = M.K, NL = M.NL;
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (long long)n * L2) return;
+  const int face = (int)(g / L2), c = (int)(g - (long long)face * L2);
+  const uint8_t* li = leaf_idx + (long long)face * leaf_stride;
+  const double* lv = M.leaves + (long long)t * K * NL * L2 + c;
+  double acc = 0.0;
+  int k = 0;
+  for (; k + 16 <= K; k += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldg(lv + ((long long)(k + u) * NL + li[k + u]) * L2);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc = dadd(acc, v[u]);
+  }
+  for (; k < K; ++k) acc = dadd(acc, __ldg(lv + ((long long)k * NL + li[k]) * L2));
+  double* cur = cur_g + (long long)face * L2 + c;
+  *cur = dadd(*cur, dmul(M.shrinkage, acc));
+}
 
 void launch_ert_level(const Launch& L, const ErtDev& M, int t, const void* frames, int u8, int w, int h,
-                      long long pitch, long long fstride, const int* face_frame, const int* boxes,
-                      int box_stride, const int* n_faces, int cap, double* cur, uint8_t* leaf_idx,
-                      int* err, int blocks) {
-  const size_t smem = ert_smem_bytes(M);
+                      long long pitch, long long fstride, const int* face_frame, const int* boxes, int box_stride,
+                      const int* n_faces, int cap, double* cur, double2* tf, uint8_t* leaf_idx,
+                      long long leaf_stride, int* err) {
+  k_ert_xform<<<(unsigned)div_up(cap, 128), 128, 0, L.st>>>(M, n_faces, cap, cur, tf, err);
+  const long long pairs = (long long)cap * M.K;
   if (u8)
-    k_ert_level<true><<<blocks, 256, smem, L.st>>>(M, t, frames, w, h, pitch, fstride, face_frame, boxes,
-                                                  box_stride, n_faces, cap, cur, leaf_idx, err);
+    k_ert_traverse<true><<<(unsigned)div_up(pairs, 256), 256, 0, L.st>>>(
+        M, t, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, cur, tf, leaf_idx, leaf_stride);
   else
-    k_ert_level<false><<<blocks, 256, smem, L.st>>>(M, t, frames, w, h, pitch, fstride, face_frame, boxes,
-                                                   box_stride, n_faces, cap, cur, leaf_idx, err);
-  ++*L.counter;
+    k_ert_traverse<false><<<(unsigned)div_up(pairs, 256), 256, 0, L.st>>>(
+        M, t, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, cur, tf, leaf_idx, leaf_stride);
+  k_ert_accum<<<(unsigned)div_up((long long)cap * 2 * M.L, 256), 256, 0, L.st>>>(M, t, n_faces, cap, cur, leaf_idx,
+                                                                                leaf_stride);
+  *L.counter += 3;
 }
 
 __global__ void k_ert_finish(ErtDev M, const int* __restrict__ boxes, int box_stride,

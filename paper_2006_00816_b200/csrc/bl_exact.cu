@@ -13,19 +13,24 @@
 
 namespace blb {
 
-// Exact separable window score; lanes 0..9 each own one window row.  Result valid in lane 0.
-BL_DEV double exact_window_score(const double* __restrict__ feat, int cw, int cx, int cy,
-                                 const double* __restrict__ w, double bias, int lane) {
+// Exact separable window score.  A warp scores three windows at once: lanes 10g..10g+9 own
+// the ten window rows of window g (g = 0, 1, 2; lanes 30-31 idle), each accumulating its
+// 310-term row dot product in the reference's order; the row sums are then added in order
+// by the group's first lane.  Result valid in lanes 0, 10, 20.
+BL_DEV double exact_window_score3(const double* __restrict__ feat, int cw, int cx, int cy,
+                                  const double* __restrict__ w, double bias, int lane, bool active) {
+  const int g = lane / 10, j = lane - 10 * (lane / 10);
   double acc = 0.0;
-  if (lane < kWin) {
-    const double* strip = feat + ((long long)(cy + lane) * cw + cx) * kFeat;
-    const double* wr = w + lane * kRowW;
+  if (active && g < 3) {
+    const double* strip = feat + ((long long)(cy + j) * cw + cx) * kFeat;
+    const double* wr = w + j * kRowW;
 #pragma unroll 10
     for (int k = 0; k < kRowW; ++k) acc = dadd(acc, dmul(__ldg(strip + k), __ldg(wr + k)));
   }
   double total = 0.0;
+  const int base = (g < 3 ? g : 0) * 10;
 #pragma unroll
-  for (int j = 0; j < kWin; ++j) total = dadd(total, __shfl_sync(0xffffffffu, acc, j));
+  for (int jj = 0; jj < kWin; ++jj) total = dadd(total, __shfl_sync(0xffffffffu, acc, base + jj));
   return dadd(total, bias);
 }
 
@@ -41,15 +46,18 @@ __global__ void __launch_bounds__(256) k_rescore(const PlanDesc* __restrict__ P,
                                                  int* __restrict__ det_count, long long cap_pf,
                                                  int* __restrict__ overflow) {
   const int lane = threadIdx.x & 31;
+  const int g = lane / 10;
   const long long n = min((long long)*n_cand, cand_cap);
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
-    const Candidate c = cand[i];
+  for (long long i0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 3; i0 < n; i0 += nw * 3) {
+    const long long i = i0 + (g < 3 ? g : 0);
+    const bool active = g < 3 && i < n;
+    const Candidate c = cand[active ? i : i0];
     const int s = c.slot_r >> 3, r = c.slot_r & 7;
     const LevelDesc& D = P->lv[s];
     const double* fb = feat64 + (D.cell_off + (long long)c.frame * D.cw * D.ch) * kFeat;
-    const double sc = exact_window_score(fb, D.cw, c.cx, c.cy, w64 + r * kFilterW, bias[r], lane);
-    if (lane == 0 && sc > thr) {  // detector.cpp:110 (strict)
+    const double sc = exact_window_score3(fb, D.cw, c.cx, c.cy, w64 + r * kFilterW, bias[r], lane, active);
+    if (active && lane == 10 * g && sc > thr) {  // detector.cpp:110 (strict)
       DevDet d;
       d.x = round_half_up(ddiv((double)(c.cx * cell_px), D.c));
       d.y = round_half_up(ddiv((double)(c.cy * cell_px), D.c));
@@ -81,13 +89,17 @@ __global__ void __launch_bounds__(256) k_score_all(const double* __restrict__ fe
                                                    const double* __restrict__ w, double bias,
                                                    double* __restrict__ scores) {
   const int lane = threadIdx.x & 31;
+  const int g = lane / 10;
   const int sw = cw - (kWin - 1), sh = ch - (kWin - 1);
   const long long n = (long long)sw * sh;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
-    const int cy = (int)(i / sw), cx = (int)(i - (long long)(i / sw) * sw);
-    const double sc = exact_window_score(feat, cw, cx, cy, w, bias, lane);
-    if (lane == 0) scores[i] = sc;
+  for (long long i0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 3; i0 < n; i0 += nw * 3) {
+    const long long i = i0 + (g < 3 ? g : 0);
+    const bool active = g < 3 && i < n;
+    const long long ii = active ? i : i0;
+    const int cy = (int)(ii / sw), cx = (int)(ii - (long long)(ii / sw) * sw);
+    const double sc = exact_window_score3(feat, cw, cx, cy, w, bias, lane, active);
+    if (active && lane == 10 * g) scores[i] = sc;
   }
 }
 

@@ -167,9 +167,9 @@ void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, 
 // bl_ert.cu
 void launch_ert_init(const Launch& L, const ErtDev& M, const int* n_faces, int cap, double* cur);
 void launch_ert_level(const Launch& L, const ErtDev& M, int t, const void* frames, int u8, int w, int h,
-                      long long pitch, long long fstride, const int* face_frame, const int* boxes,
-                      int box_stride, const int* n_faces, int cap, double* cur, uint8_t* leaf_idx,
-                      int* err, int blocks);
+                      long long pitch, long long fstride, const int* face_frame, const int* boxes, int box_stride,
+                      const int* n_faces, int cap, double* cur, double2* tf, uint8_t* leaf_idx,
+                      long long leaf_stride, int* err);
 void launch_ert_finish(const Launch& L, const ErtDev& M, const int* boxes, int box_stride,
                        const int* n_faces, int cap, const double* cur, double* out_xy);
 

@@ -12,54 +12,59 @@
 
 namespace blb {
 
+constexpr int kRsRows = 4;  // output rows per thread (column terms computed once)
+
 template <typename Tin>
 __global__ void __launch_bounds__(256) k_resample(const Tin* __restrict__ src, int sw, int sh,
                                                   long long s_pitch, long long s_fstride,
                                                   double* __restrict__ dst, int dw, int dh,
-                                                  long long d_fstride) {
+                                                  long long d_fstride, double rx, double ry) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  if (x >= dw || y >= dh) return;
+  const int y_first = (blockIdx.y * blockDim.y + threadIdx.y) * kRsRows;
+  if (x >= dw || y_first >= dh) return;
   const Tin* s = src + (long long)blockIdx.z * s_fstride;
-  // image.cpp:136-137
-  const double rx = ddiv((double)sw, (double)dw);
-  const double ry = ddiv((double)sh, (double)dh);
-  // image.cpp:139-143
-  double sy = dsub(dmul(dadd((double)y, 0.5), ry), 0.5);
-  const double ymax = (double)(sh - 1);
-  sy = sy < 0.0 ? 0.0 : (ymax < sy ? ymax : sy);
-  const int y0 = (int)sy;
-  const int y1 = min(y0 + 1, sh - 1);
-  const double fy = dsub(sy, (double)y0);
-  // image.cpp:145-149
+  double* d = dst + (long long)blockIdx.z * d_fstride;
+  // image.cpp:145-149 (rx = double(w)/dw is computed on the host, the same IEEE division)
   double sx = dsub(dmul(dadd((double)x, 0.5), rx), 0.5);
   const double xmax = (double)(sw - 1);
   sx = sx < 0.0 ? 0.0 : (xmax < sx ? xmax : sx);
   const int x0 = (int)sx;
   const int x1 = min(x0 + 1, sw - 1);
   const double fx = dsub(sx, (double)x0);
-  // image.cpp:150-152
-  const double a = (double)__ldg(s + y0 * s_pitch + x0);
-  const double b = (double)__ldg(s + y0 * s_pitch + x1);
-  const double c = (double)__ldg(s + y1 * s_pitch + x0);
-  const double d = (double)__ldg(s + y1 * s_pitch + x1);
   const double gx = dsub(1.0, fx);
-  const double top = dadd(dmul(a, gx), dmul(b, fx));
-  const double bot = dadd(dmul(c, gx), dmul(d, fx));
-  dst[(long long)blockIdx.z * d_fstride + (long long)y * dw + x] =
-      dadd(dmul(top, dsub(1.0, fy)), dmul(bot, fy));
+  const double ymax = (double)(sh - 1);
+#pragma unroll
+  for (int j = 0; j < kRsRows; ++j) {
+    const int y = y_first + j;
+    if (y >= dh) break;
+    // image.cpp:139-143
+    double sy = dsub(dmul(dadd((double)y, 0.5), ry), 0.5);
+    sy = sy < 0.0 ? 0.0 : (ymax < sy ? ymax : sy);
+    const int y0 = (int)sy;
+    const int y1 = min(y0 + 1, sh - 1);
+    const double fy = dsub(sy, (double)y0);
+    // image.cpp:150-152
+    const double a = (double)__ldg(s + y0 * s_pitch + x0);
+    const double b = (double)__ldg(s + y0 * s_pitch + x1);
+    const double c = (double)__ldg(s + y1 * s_pitch + x0);
+    const double e = (double)__ldg(s + y1 * s_pitch + x1);
+    const double top = dadd(dmul(a, gx), dmul(b, fx));
+    const double bot = dadd(dmul(c, gx), dmul(e, fx));
+    d[(long long)y * dw + x] = dadd(dmul(top, dsub(1.0, fy)), dmul(bot, fy));
+  }
 }
 
 void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
                      long long s_fstride, double* dst, int dw, int dh, long long d_fstride, int n) {
+  const double rx = double(sw) / dw, ry = double(sh) / dh;  // image.cpp:136-137
   const dim3 block(32, 8);
-  const dim3 grid((unsigned)div_up(dw, 32), (unsigned)div_up(dh, 8), (unsigned)n);
+  const dim3 grid((unsigned)div_up(dw, 32), (unsigned)div_up(dh, 8 * kRsRows), (unsigned)n);
   if (src_u8)
-    k_resample<uint8_t><<<grid, block, 0, L.st>>>((const uint8_t*)src, sw, sh, s_pitch, s_fstride,
-                                                   dst, dw, dh, d_fstride);
+    k_resample<uint8_t><<<grid, block, 0, L.st>>>((const uint8_t*)src, sw, sh, s_pitch, s_fstride, dst, dw, dh,
+                                                   d_fstride, rx, ry);
   else
-    k_resample<double><<<grid, block, 0, L.st>>>((const double*)src, sw, sh, s_pitch, s_fstride, dst,
-                                                  dw, dh, d_fstride);
+    k_resample<double><<<grid, block, 0, L.st>>>((const double*)src, sw, sh, s_pitch, s_fstride, dst, dw, dh,
+                                                  d_fstride, rx, ry);
   ++*L.counter;
 }
 
