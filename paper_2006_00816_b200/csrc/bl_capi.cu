@@ -116,7 +116,7 @@ struct DetectorState {
 struct ErtState {
   bool ready = false;
   ErtDev dev{};
-  DevBuf mean, anchors, split, leaves;
+  DevBuf mean, mean_c, split, leaves;
 };
 
 // A batch plan: geometry + device arenas for (n, w, h, pixel type, detector geometry).
@@ -451,9 +451,9 @@ int run_ert(bl_ctx* c, const void* frames, int pix, int w, int h, long long pitc
   long long leaf_stride = (long long)E.dev.T * E.dev.K;
   uint8_t* leaf = leaf_dev;
   if (!leaf) {
-    TRY(c->ert_leafs.ensure((size_t)std::max(1, nf) * E.dev.K + 16));
+    leaf_stride = div_up(E.dev.K, 16) * 16;  // 16-B aligned rows: 128-bit index loads
+    TRY(c->ert_leafs.ensure((size_t)std::max(1, nf) * leaf_stride + 16));
     leaf = c->ert_leafs.as<uint8_t>();
-    leaf_stride = E.dev.K;
   }
   CK(cudaMemsetAsync(c->ert_err.p, 0, sizeof(int), c->st));
   launch_ert_init(L, E.dev, n_faces_dev, nf, c->ert_cur.as<double>());
@@ -789,20 +789,33 @@ int bl_ert_upload(bl_ctx* c, int L, int T, int K, int F, double shrinkage, const
   E.ready = false;
   const int S = (1 << F) - 1, NL = 1 << F;
   const size_t nsplit = (size_t)T * K * S;
-  std::vector<int16_t> a16(2 * nsplit + 2);
-  for (size_t i = 0; i < 2 * nsplit; ++i) {
-    if (anchors[i] < 0 || anchors[i] >= L) return set_err(BL_ERR_MODEL, "split anchor out of range");
-    a16[i] = (int16_t)anchors[i];
-  }
+  if (2 * L > 512) return set_err(BL_ERR_MODEL, "landmark count above 256 is not supported");
+  // node-major split records [t][node][k] (tree-major in the upload format)
+  std::vector<SplitRec> recs(nsplit + 1);
+  for (int t = 0; t < T; ++t)
+    for (int k = 0; k < K; ++k)
+      for (int s = 0; s < S; ++s) {
+        const size_t src = ((size_t)t * K + k) * S + s;
+        const int32_t a = anchors[2 * src], b = anchors[2 * src + 1];
+        if (a < 0 || a >= L || b < 0 || b >= L) return set_err(BL_ERR_MODEL, "split anchor out of range");
+        SplitRec& r = recs[((size_t)t * S + s) * K + k];
+        r.oax = split_params[5 * src];
+        r.oay = split_params[5 * src + 1];
+        r.obx = split_params[5 * src + 2];
+        r.oby = split_params[5 * src + 3];
+        r.thr = split_params[5 * src + 4];
+        r.anchors = make_short2((short)a, (short)b);
+        r.pad = 0;
+      }
   TRY(E.mean.ensure(sizeof(double) * 2 * L));
-  TRY(E.anchors.ensure(sizeof(int16_t) * a16.size()));
-  TRY(E.split.ensure(sizeof(double) * 5 * nsplit + 8));
-  TRY(E.leaves.ensure(sizeof(double) * (size_t)T * K * NL * L * 2 + 8));
+  TRY(E.mean_c.ensure(sizeof(double) * 2 * L));
+  TRY(E.split.ensure(sizeof(SplitRec) * recs.size()));
+  TRY(E.leaves.ensure(sizeof(double) * (size_t)T * K * NL * L * 2 + 16));
   CK(cudaMemcpy(E.mean.p, mean_xy, sizeof(double) * 2 * L, cudaMemcpyDefault));
-  CK(cudaMemcpy(E.anchors.p, a16.data(), sizeof(int16_t) * a16.size(), cudaMemcpyHostToDevice));
-  if (nsplit) CK(cudaMemcpy(E.split.p, split_params, sizeof(double) * 5 * nsplit, cudaMemcpyDefault));
+  CK(cudaMemcpy(E.split.p, recs.data(), sizeof(SplitRec) * recs.size(), cudaMemcpyHostToDevice));
   if ((size_t)T * K) CK(cudaMemcpy(E.leaves.p, leaves, sizeof(double) * (size_t)T * K * NL * L * 2, cudaMemcpyDefault));
-  // centroid of the mean shape in similarity_transform's order (ert.cpp:33-43)
+  // centroid of the mean shape in similarity_transform's order (ert.cpp:33-43), and the
+  // centred mean (to.x - mt.x, to.y - mt.y) every level reuses
   std::vector<double> m(2 * L);
   CK(cudaMemcpy(m.data(), mean_xy, sizeof(double) * 2 * L, cudaMemcpyDefault));
   double mx = 0, my = 0;
@@ -812,6 +825,12 @@ int bl_ert_upload(bl_ctx* c, int L, int T, int K, int F, double shrinkage, const
   }
   mx /= double(L);
   my /= double(L);
+  std::vector<double> mc(2 * L);
+  for (int i = 0; i < L; ++i) {
+    mc[2 * i] = m[2 * i] - mx;
+    mc[2 * i + 1] = m[2 * i + 1] - my;
+  }
+  CK(cudaMemcpy(E.mean_c.p, mc.data(), sizeof(double) * 2 * L, cudaMemcpyHostToDevice));
   E.dev.L = L;
   E.dev.T = T;
   E.dev.K = K;
@@ -820,8 +839,8 @@ int bl_ert_upload(bl_ctx* c, int L, int T, int K, int F, double shrinkage, const
   E.dev.NL = NL;
   E.dev.shrinkage = shrinkage;
   E.dev.mean_xy = E.mean.as<double>();
-  E.dev.anchors = E.anchors.as<int16_t>();
-  E.dev.split = E.split.as<double>();
+  E.dev.mean_c = E.mean_c.as<double>();
+  E.dev.split = E.split.as<SplitRec>();
   E.dev.leaves = E.leaves.as<double>();
   E.dev.mean_cx = mx;
   E.dev.mean_cy = my;

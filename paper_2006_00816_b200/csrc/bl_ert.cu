@@ -15,6 +15,8 @@
 // Level-synchronous launches keep one level's trees (K * 2^F * L * 16 B = 8.7 MB at 500
 // trees, depth 4, L = 68) resident in L2 for every face of the batch: HBM reads the model
 // once per batch; L2 serves the 1088-B leaf row each (face, tree) selects.
+#include <stdint.h>
+
 #include "bl_internal.cuh"
 
 namespace blb {
@@ -50,29 +52,40 @@ BL_DEV double sample_px(const void* fr, int w, int h, long long pitch, int bx, i
   return __ldg((const double*)fr + (long long)iy * pitch + ix);
 }
 
-// (1) similarity_transform(current, mean) per face, ert.cpp:26-69: sequential sums in the
+// (1) similarity_transform(current, mean) per face, ert.cpp:26-69.  A warp per face stages
+// the current shape in shared memory; lane 0 then runs the sums sequentially in the
 // reference's order (bit-identical), then CUDA hypot/atan2/cos/sin.  Stores the linear part
 // (scale*cos, scale*sin) that apply_linear recomputes for every sample (ert.cpp:21-22).
-__global__ void __launch_bounds__(128) k_ert_xform(ErtDev M, const int* __restrict__ n_faces, int cap,
-                                                   const double* __restrict__ cur_g, double2* __restrict__ tf,
-                                                   int* __restrict__ err) {
+constexpr int kXfFaces = 4;
+constexpr int kMaxL2 = 512;  // 2L <= 512 (L <= 256) for the staged kernels
+
+__global__ void __launch_bounds__(32 * kXfFaces) k_ert_xform(ErtDev M, const int* __restrict__ n_faces, int cap,
+                                                             const double* __restrict__ cur_g,
+                                                             double2* __restrict__ tf, int* __restrict__ err) {
+  __shared__ double sc[kXfFaces][kMaxL2];
   const int n = min(*n_faces, cap);
-  const int face = blockIdx.x * blockDim.x + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int face = blockIdx.x * kXfFaces + warp;
   if (face >= n) return;
-  const double* cur = cur_g + (long long)face * 2 * M.L;
+  const int L = M.L, L2 = 2 * L;
+  const double* cur = cur_g + (long long)face * L2;
+  for (int i = lane; i < L2; i += 32) sc[warp][i] = cur[i];
+  __syncwarp();
+  if (lane != 0) return;
+  const double* c = sc[warp];
   double mfx = 0.0, mfy = 0.0;
-  for (int i = 0; i < M.L; ++i) {
-    mfx = dadd(mfx, cur[2 * i]);
-    mfy = dadd(mfy, cur[2 * i + 1]);
+  for (int i = 0; i < L; ++i) {
+    mfx = dadd(mfx, c[2 * i]);
+    mfy = dadd(mfy, c[2 * i + 1]);
   }
-  mfx = ddiv(mfx, (double)M.L);
-  mfy = ddiv(mfy, (double)M.L);
+  mfx = ddiv(mfx, (double)L);
+  mfy = ddiv(mfy, (double)L);
   double sff = 0.0, sre = 0.0, sim = 0.0;
-  for (int i = 0; i < M.L; ++i) {
-    const double fx = dsub(cur[2 * i], mfx);
-    const double fy = dsub(cur[2 * i + 1], mfy);
-    const double txp = dsub(__ldg(M.mean_xy + 2 * i), M.mean_cx);
-    const double typ = dsub(__ldg(M.mean_xy + 2 * i + 1), M.mean_cy);
+  for (int i = 0; i < L; ++i) {
+    const double fx = dsub(c[2 * i], mfx);
+    const double fy = dsub(c[2 * i + 1], mfy);
+    const double txp = __ldg(M.mean_c + 2 * i);  // to.x - mt.x, host-computed with the same op
+    const double typ = __ldg(M.mean_c + 2 * i + 1);
     sff = dadd(sff, dadd(dmul(fx, fx), dmul(fy, fy)));
     sre = dadd(sre, dadd(dmul(fx, txp), dmul(fy, typ)));
     sim = dadd(sim, dsub(dmul(fx, typ), dmul(fy, txp)));
@@ -94,8 +107,9 @@ __global__ void __launch_bounds__(128) k_ert_xform(ErtDev M, const int* __restri
   tf[face] = make_double2(A, B);
 }
 
-// (2) one thread per (face, tree): traverse_tree (ert.cpp:87-97) with sample_intensity
-// (ert.cpp:71-85) on the ORIGINAL frame; writes the leaf index.
+// (2) one CTA per face, one thread per tree: traverse_tree (ert.cpp:87-97) with
+// sample_intensity (ert.cpp:71-85) on the ORIGINAL frame; the face's current shape is staged
+// in shared memory; split records are node-major so a warp's loads are contiguous.
 template <bool U8>
 __global__ void __launch_bounds__(256) k_ert_traverse(ErtDev M, int t, const void* __restrict__ frames, int w,
                                                       int h, long long pitch, long long fstride,
@@ -105,71 +119,96 @@ __global__ void __launch_bounds__(256) k_ert_traverse(ErtDev M, int t, const voi
                                                       const double* __restrict__ cur_g,
                                                       const double2* __restrict__ tf,
                                                       uint8_t* __restrict__ leaf_idx, long long leaf_stride) {
+  __shared__ double sc[kMaxL2];
   const int n = min(*n_faces, cap);
-  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int K = M.K, S = M.S;
-  if (g >= (long long)n * K) return;
-  const int face = (int)(g / K), k = (int)(g - (long long)face * K);
+  const int face = blockIdx.x;
+  if (face >= n) return;
+  const int K = M.K, S = M.S, L2 = 2 * M.L;
+  const double* cur = cur_g + (long long)face * L2;
+  for (int i = threadIdx.x; i < L2; i += blockDim.x) sc[i] = cur[i];
+  __syncthreads();
   const double2 ab = tf[face];
-  const double* cur = cur_g + (long long)face * 2 * M.L;
   const int* bx = boxes + (long long)face * box_stride;
   const int X = bx[0], Y = bx[1], W = bx[2], H = bx[3];
   const void* fr = (const char*)frames + (long long)face_frame[face] * fstride * (U8 ? 1 : 8);
-  const long long tree = (long long)t * K + k;
-  int node = 0;
-  while (node < S) {
-    const long long sn = tree * S + node;
-    const short2 an = *reinterpret_cast<const short2*>(M.anchors + 2 * sn);
-    const double* sp = M.split + 5 * sn;
-    const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, cur, ab.x, ab.y, an.x, __ldg(sp), __ldg(sp + 1));
-    const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, cur, ab.x, ab.y, an.y, __ldg(sp + 2), __ldg(sp + 3));
-    node = dsub(ia, ib) > __ldg(sp + 4) ? 2 * node + 1 : 2 * node + 2;
+  const SplitRec* lvl = M.split + (long long)t * S * K;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    int node = 0;
+    while (node < S) {
+      const SplitRec* r = lvl + (long long)node * K + k;
+      const double2 oa = __ldg(reinterpret_cast<const double2*>(r));      // offset_a
+      const double2 ob = __ldg(reinterpret_cast<const double2*>(r) + 1);  // offset_b
+      const int4 tail = __ldg(reinterpret_cast<const int4*>(r) + 2);      // thr, anchors
+      const double thr = __hiloint2double(tail.y, tail.x);
+      const int an_a = (short)(tail.z & 0xffff), an_b = (short)(tail.z >> 16);
+      const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_a, oa.x, oa.y);
+      const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_b, ob.x, ob.y);
+      node = dsub(ia, ib) > thr ? 2 * node + 1 : 2 * node + 2;
+    }
+    leaf_idx[(long long)face * leaf_stride + k] = (uint8_t)(node - S);
   }
-  leaf_idx[(long long)face * leaf_stride + k] = (uint8_t)(node - S);
 }
 
-// (3) one thread per (face, coordinate): sum the K selected leaf rows IN TREE ORDER in fp64
-// (ert.cpp:118-121), then cur += shrinkage * delta (ert.cpp:123-126).  Consecutive threads
-// read consecutive coordinates of one leaf row (coalesced, L2-resident for the level); the
-// loads of 16 trees are issued ahead of their adds.
+// (3) one thread per (face, landmark): sums the K selected leaf rows IN TREE ORDER in fp64
+// (ert.cpp:118-121) for the landmark's (x, y) pair, then cur += shrinkage * delta
+// (ert.cpp:123-126).  Consecutive threads read consecutive 16-B pairs of one leaf row
+// (coalesced, L2-resident for the level); 16 leaf indices arrive per 128-bit load and the
+// 16 trees' loads are issued ahead of their adds.
 __global__ void __launch_bounds__(256) k_ert_accum(ErtDev M, int t, const int* __restrict__ n_faces, int cap,
                                                    double* __restrict__ cur_g,
                                                    const uint8_t* __restrict__ leaf_idx, long long leaf_stride) {
   const int n = min(*n_faces, cap);
-  const int L2 = 2 * M.L, K = M.K, NL = M.NL;
+  const int L = M.L, K = M.K, NL = M.NL;
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= (long long)n * L2) return;
-  const int face = (int)(g / L2), c = (int)(g - (long long)face * L2);
+  if (g >= (long long)n * L) return;
+  const int face = (int)(g / L), p = (int)(g - (long long)face * L);
   const uint8_t* li = leaf_idx + (long long)face * leaf_stride;
-  const double* lv = M.leaves + (long long)t * K * NL * L2 + c;
-  double acc = 0.0;
+  const double2* lv = reinterpret_cast<const double2*>(M.leaves + (long long)t * K * NL * 2 * L) + p;
+  const int row = NL * L;  // double2 per tree
+  double ax = 0.0, ay = 0.0;
   int k = 0;
-  for (; k + 16 <= K; k += 16) {
-    double v[16];
+  const bool vec = ((reinterpret_cast<uintptr_t>(li) & 15) == 0);
+  for (; vec && k + 16 <= K; k += 16) {
+    const uint4 q = *reinterpret_cast<const uint4*>(li + k);
+    const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+    double2 v[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) v[u] = __ldg(lv + ((long long)(k + u) * NL + li[k + u]) * L2);
+    for (int u = 0; u < 16; ++u) {
+      const int idx = (wv[u >> 2] >> ((u & 3) * 8)) & 0xff;
+      v[u] = __ldg(lv + (k + u) * row + idx * L);
+    }
 #pragma unroll
-    for (int u = 0; u < 16; ++u) acc = dadd(acc, v[u]);
+    for (int u = 0; u < 16; ++u) {
+      ax = dadd(ax, v[u].x);
+      ay = dadd(ay, v[u].y);
+    }
   }
-  for (; k < K; ++k) acc = dadd(acc, __ldg(lv + ((long long)k * NL + li[k]) * L2));
-  double* cur = cur_g + (long long)face * L2 + c;
-  *cur = dadd(*cur, dmul(M.shrinkage, acc));
+  for (; k < K; ++k) {
+    const double2 v = __ldg(lv + k * row + li[k] * L);
+    ax = dadd(ax, v.x);
+    ay = dadd(ay, v.y);
+  }
+  double2* cur = reinterpret_cast<double2*>(cur_g + (long long)face * 2 * L) + p;
+  double2 cv = *cur;
+  cv.x = dadd(cv.x, dmul(M.shrinkage, ax));
+  cv.y = dadd(cv.y, dmul(M.shrinkage, ay));
+  *cur = cv;
 }
 
 void launch_ert_level(const Launch& L, const ErtDev& M, int t, const void* frames, int u8, int w, int h,
                       long long pitch, long long fstride, const int* face_frame, const int* boxes, int box_stride,
                       const int* n_faces, int cap, double* cur, double2* tf, uint8_t* leaf_idx,
                       long long leaf_stride, int* err) {
-  k_ert_xform<<<(unsigned)div_up(cap, 128), 128, 0, L.st>>>(M, n_faces, cap, cur, tf, err);
-  const long long pairs = (long long)cap * M.K;
+  k_ert_xform<<<(unsigned)div_up(cap, kXfFaces), 32 * kXfFaces, 0, L.st>>>(M, n_faces, cap, cur, tf, err);
+  const int tb = M.K >= 256 ? 256 : (int)div_up(M.K, 32) * 32;
   if (u8)
-    k_ert_traverse<true><<<(unsigned)div_up(pairs, 256), 256, 0, L.st>>>(
-        M, t, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, cur, tf, leaf_idx, leaf_stride);
+    k_ert_traverse<true><<<(unsigned)cap, tb, 0, L.st>>>(M, t, frames, w, h, pitch, fstride, face_frame, boxes,
+                                                        box_stride, n_faces, cap, cur, tf, leaf_idx, leaf_stride);
   else
-    k_ert_traverse<false><<<(unsigned)div_up(pairs, 256), 256, 0, L.st>>>(
-        M, t, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, cur, tf, leaf_idx, leaf_stride);
-  k_ert_accum<<<(unsigned)div_up((long long)cap * 2 * M.L, 256), 256, 0, L.st>>>(M, t, n_faces, cap, cur, leaf_idx,
-                                                                                leaf_stride);
+    k_ert_traverse<false><<<(unsigned)cap, tb, 0, L.st>>>(M, t, frames, w, h, pitch, fstride, face_frame, boxes,
+                                                         box_stride, n_faces, cap, cur, tf, leaf_idx, leaf_stride);
+  k_ert_accum<<<(unsigned)div_up((long long)cap * M.L, 256), 256, 0, L.st>>>(M, t, n_faces, cap, cur, leaf_idx,
+                                                                           leaf_stride);
   *L.counter += 3;
 }
 

@@ -103,12 +103,21 @@ struct DevDet {
 };
 static_assert(sizeof(DevDet) == sizeof(bl_detection), "layout");
 
+// One split node, 48 B (three 16-B loads).  Stored node-major, [t][node][k], so the lanes of
+// a warp (consecutive trees k) read consecutive records.
+struct SplitRec {
+  double oax, oay, obx, oby, thr;
+  short2 anchors;
+  int pad;
+};
+static_assert(sizeof(SplitRec) == 48, "split record layout");
+
 struct ErtDev {
   int L, T, K, F, S, NL;
   double shrinkage;
   const double* mean_xy;      // L*2
-  const int16_t* anchors;     // T*K*S*2
-  const double* split;        // T*K*S*5
+  const double* mean_c;       // L*2: mean shape minus its centroid (ert.cpp:41-46 txp/typ)
+  const SplitRec* split;      // [T][S][K]
   const double* leaves;       // T*K*NL*L*2
   double mean_cx, mean_cy;    // centroid of the mean shape (host-computed, ert.cpp:33-43 order)
 };
