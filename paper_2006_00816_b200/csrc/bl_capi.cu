@@ -258,8 +258,20 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
     L.cell_off = cells;
     L.cell_begin = cells;
     cells += (long long)n * L.cw * L.ch;
-    L.cw_pad = (int)(div_up(L.sw, kTileAX) * kTileAX + 12);
-    L.ch_pad = (int)(div_up(L.sh, kTileAY) * kTileAY + (kWin - 1));
+    {  // screening tile shape with the least padding
+      long long best = -1;
+      for (int lx : {8, 4, 2}) {
+        const long long tw = 4 * lx, th = 32 / lx;
+        const long long area = div_up(L.sw, tw) * tw * div_up(L.sh, th) * th;
+        if (best < 0 || area < best) {
+          best = area;
+          L.sc_lanes_x = lx;
+        }
+      }
+    }
+    const int tile_w = 4 * L.sc_lanes_x, tile_h = 32 / L.sc_lanes_x;
+    L.cw_pad = (int)(div_up(L.sw, tile_w) * tile_w + 12);
+    L.ch_pad = (int)(div_up(L.sh, tile_h) * tile_h + (kWin - 1));
     L.f32_off = f32;
     L.f32_fstride = (long long)kFeatPad * L.ch_pad * L.cw_pad;
     f32 += (long long)n * L.f32_fstride;
@@ -273,8 +285,8 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
     L.gh_tiles_y = (int)div_up(L.ch, kGhSegRows);
     L.gh_begin = gh;
     gh += (long long)n * L.gh_tiles_x * L.gh_tiles_y;
-    L.sc_tiles_x = (int)div_up(L.sw, kTileAX);
-    L.sc_tiles_y = (int)div_up(L.sh, kTileAY);
+    L.sc_tiles_x = (int)div_up(L.sw, tile_w);
+    L.sc_tiles_y = (int)div_up(L.sh, tile_h);
     L.sc_begin = sc;
     sc += (long long)n * L.sc_tiles_x * L.sc_tiles_y;
     L.anchor_base = anchors_pf;

@@ -47,8 +47,9 @@ __global__ void __launch_bounds__(kScreenWarps * 32, 2) k_screen(const PlanDesc*
   const int tiles = D.sc_tiles_x * D.sc_tiles_y;
   const int f = (int)(local / tiles);
   const int t = (int)(local - (long long)f * tiles);
-  const int x = (t % D.sc_tiles_x) * kTileAX + (lane & 7) * 4;
-  const int y = (t / D.sc_tiles_x) * kTileAY + (lane >> 3);
+  const int lx = D.sc_lanes_x;
+  const int x = (t % D.sc_tiles_x) * (4 * lx) + (lane % lx) * 4;
+  const int y = (t / D.sc_tiles_x) * (32 / lx) + lane / lx;
   const int cw_pad = D.cw_pad;
   const long long plane = (long long)D.ch_pad * cw_pad;
   const float* fb = feat32 + D.f32_off + (long long)f * D.f32_fstride + x;
@@ -59,11 +60,37 @@ __global__ void __launch_bounds__(kScreenWarps * 32, 2) k_screen(const PlanDesc*
 #pragma unroll
     for (int r = 0; r < kFilters; ++r) acc[q][r] = 0.f;
 
-  // software pipeline: the next (j, f) feature vectors are in flight while the current
-  // ones feed 200 FMAs
-  const float* rowp0 = fb + (long long)y * cw_pad;
-  float4 n0 = __ldg(reinterpret_cast<const float4*>(rowp0)), n1 = __ldg(reinterpret_cast<const float4*>(rowp0) + 1),
-         n2 = __ldg(reinterpret_cast<const float4*>(rowp0) + 2), n3 = __ldg(reinterpret_cast<const float4*>(rowp0) + 3);
+  // software pipeline: feature vectors of step (j, f+1) are in flight while step (j, f) feeds
+  // 200 FMAs; the f loop is unrolled by two so the two prefetch buffers alternate by name.
+  auto load4 = [&](int j, int ff, float4& a0, float4& a1, float4& a2, float4& a3) {
+    const float4* p = reinterpret_cast<const float4*>(fb + (long long)(y + j) * cw_pad + ff * plane);
+    a0 = __ldg(p);
+    a1 = __ldg(p + 1);
+    a2 = __ldg(p + 2);
+    a3 = __ldg(p + 3);
+  };
+  auto step = [&](float (&aj)[4][kFilters], const float4& a0, const float4& a1, const float4& a2, const float4& a3,
+                  const float4* wp) {
+    const float v[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
+                         a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
+    float wv[kWBlock];
+#pragma unroll
+    for (int k = 0; k < kWBlock / 4; ++k) {
+      const float4 t4 = wp[k];
+      wv[4 * k] = t4.x;
+      wv[4 * k + 1] = t4.y;
+      wv[4 * k + 2] = t4.z;
+      wv[4 * k + 3] = t4.w;
+    }
+#pragma unroll
+    for (int i = 0; i < kWin; ++i)
+#pragma unroll
+      for (int r = 0; r < kFilters; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) aj[q][r] = fmaf(v[q + i], wv[i * kFilters + r], aj[q][r]);
+  };
+  float4 p0, p1, p2, p3, q0, q1, q2, q3;
+  load4(0, 0, p0, p1, p2, p3);
 #pragma unroll 1
   for (int j = 0; j < kWin; ++j) {
     float aj[4][kFilters];
@@ -72,35 +99,22 @@ __global__ void __launch_bounds__(kScreenWarps * 32, 2) k_screen(const PlanDesc*
 #pragma unroll
       for (int r = 0; r < kFilters; ++r) aj[q][r] = 0.f;
     const float4* wj = sW4 + j * kFeat * (kWBlock / 4);
+    // kFeat = 31 = 15 pairs + 1
 #pragma unroll 1
-    for (int ff = 0; ff < kFeat; ++ff) {
-      const float v[16] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w,
-                           n2.x, n2.y, n2.z, n2.w, n3.x, n3.y, n3.z, n3.w};
-      {  // prefetch (j, ff+1), or (j+1, 0); the last prefetch re-reads row y+9, harmlessly
-        const int nf = ff + 1 < kFeat ? ff + 1 : 0;
-        const int nj = ff + 1 < kFeat ? j : min(j + 1, kWin - 1);
-        const float4* p = reinterpret_cast<const float4*>(fb + (long long)(y + nj) * cw_pad + nf * plane);
-        n0 = __ldg(p);
-        n1 = __ldg(p + 1);
-        n2 = __ldg(p + 2);
-        n3 = __ldg(p + 3);
-      }
-      const float4* wp = wj + ff * (kWBlock / 4);
-      float wv[kWBlock];
-#pragma unroll
-      for (int k = 0; k < kWBlock / 4; ++k) {
-        const float4 t4 = wp[k];
-        wv[4 * k] = t4.x;
-        wv[4 * k + 1] = t4.y;
-        wv[4 * k + 2] = t4.z;
-        wv[4 * k + 3] = t4.w;
-      }
-#pragma unroll
-      for (int i = 0; i < kWin; ++i)
-#pragma unroll
-        for (int r = 0; r < kFilters; ++r)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) aj[q][r] = fmaf(v[q + i], wv[i * kFilters + r], aj[q][r]);
+    for (int ff = 0; ff < kFeat - 1; ff += 2) {
+      load4(j, ff + 1, q0, q1, q2, q3);
+      step(aj, p0, p1, p2, p3, wj + ff * (kWBlock / 4));
+      const int nf = ff + 2;  // < kFeat
+      load4(j, nf, p0, p1, p2, p3);
+      step(aj, q0, q1, q2, q3, wj + (ff + 1) * (kWBlock / 4));
+    }
+    {  // f = 30, prefetch (j+1, 0); the last prefetch re-reads row y+9, harmlessly
+      load4(min(j + 1, kWin - 1), 0, q0, q1, q2, q3);
+      step(aj, p0, p1, p2, p3, wj + (kFeat - 1) * (kWBlock / 4));
+      p0 = q0;
+      p1 = q1;
+      p2 = q2;
+      p3 = q3;
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)

@@ -26,11 +26,9 @@ constexpr int kFilterW = kWin * kRowW;  // 3100
 constexpr int kFilters = 5;
 constexpr int kMaxLevels = 32;
 
-// Screening tile: a warp scores a 32 x 4 block of anchors (8 lanes x 4 anchors along x,
-// 4 rows), all 5 filters.  Feature planes are padded so its float4 loads never go out of
-// bounds.
-constexpr int kTileAX = 32;
-constexpr int kTileAY = 4;
+// Screening tile: a warp scores 128 anchors, 4 consecutive anchors along x per lane, all 5
+// filters; per level the tile is 32x4, 16x8 or 8x16 anchors, whichever wastes least.
+// Feature planes are padded so its float4 loads never go out of bounds.
 
 // gradHist: a warp owns 31 cells of a cell-row strip over a segment of kGhSegRows cell rows.
 constexpr int kGhCells = 31;
@@ -57,6 +55,8 @@ struct LevelDesc {
   int gh_tiles_x, gh_tiles_y;  // gradHist warp tiles per frame
   long long gh_begin;          // first gradHist warp-tile id of this level
   int sc_tiles_x, sc_tiles_y;  // screening warp tiles per frame
+  int sc_lanes_x;              // lanes along x in a screening warp tile (8, 4 or 2): tile is
+                               // (4 * sc_lanes_x) x (32 / sc_lanes_x) anchors
   long long sc_begin;          // first screening warp-tile id of this level
   long long cell_begin;        // first cell id (for per-cell kernels) of this level
   long long anchor_base;       // per-frame anchor offset (for candidate records)
