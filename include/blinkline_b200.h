@@ -132,6 +132,21 @@ int bl_detect_landmarks(bl_ctx* ctx, const void* frames, int pixel_type, int n, 
                         size_t pitch, size_t frame_stride, bl_detection* out, int64_t cap,
                         int32_t* counts, int64_t* total, double* landmarks);
 
+/* Pipelined mode (the paper's pipelined CPU/GPU model; the reference's
+ * pipelined run(), pipeline.cpp:230-324): bl_submit enqueues a batch (H2D of host frames on
+ * a copy stream, the whole detect [+ landmark] pipeline on the compute stream, result
+ * metadata back) and returns at once; bl_collect waits for it and copies its results out
+ * exactly like bl_detect / bl_detect_landmarks.  Up to two batches may be in flight, so the
+ * next batch's H2D and the previous batch's result copies overlap compute.  Tickets are
+ * collected in submission order. */
+int bl_submit(bl_ctx* ctx, const void* frames, int pixel_type, int n, int w, int h, size_t pitch,
+              size_t frame_stride, int with_landmarks, uint64_t* ticket);
+int bl_collect(bl_ctx* ctx, uint64_t ticket, bl_detection* out, int64_t cap, int32_t* counts,
+               int64_t* total, double* landmarks);
+/* Device capacity of landmarked faces per frame for the landmark pipelines (default 64); the
+ * synchronous calls grow it automatically, bl_collect reports BL_ERR_CAPACITY. */
+int bl_ctx_set_face_capacity(bl_ctx* ctx, int faces_per_frame);
+
 /* ----------------------------------------------------------- stage functions ---- */
 /* Device implementations of the reference's stage API, for the drop-in C++ layer and the
  * per-stage parity tests.  All buffers may be host or device memory. */

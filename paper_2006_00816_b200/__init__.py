@@ -83,6 +83,9 @@ _SIGS = {
     "bl_detector_upload": (C.c_int, [_vp, _vp, _vp, _dbl, C.c_int, C.c_int, C.c_int, C.c_int, _dbl]),
     "bl_ert_upload": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _dbl, _vp, _vp, _vp, _vp]),
     "bl_detect": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _sz, _sz, _vp, _i64, _vp, _P(_i64)]),
+    "bl_submit": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _sz, _sz, C.c_int, _P(_u64)]),
+    "bl_collect": (C.c_int, [_vp, _u64, _vp, _i64, _vp, _P(_i64), _vp]),
+    "bl_ctx_set_face_capacity": (C.c_int, [_vp, C.c_int]),
     "bl_landmarks": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _sz, _sz, _vp, _vp, _i64, _vp, _vp]),
     "bl_detect_landmarks": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _sz, _sz, _vp, _i64, _vp,
                                       _P(_i64), _vp]),
@@ -167,6 +170,7 @@ class Context:
         self._h = h
         self.device = device
         self._lock = threading.Lock()
+        self._inflight = {}
         self.ert_L = None
 
     def close(self):
@@ -222,43 +226,79 @@ class Context:
         self.ert_TK = int(ert["T"]) * int(ert["K"])
 
     # -------------------------------------------------------------- hot path
-    def detect(self, frames, cap=None):
-        """detect_faces over a batch -> list of DET_DTYPE arrays (one per frame)."""
-        a, pix, n, h, w = _frames(frames)
-        cap = cap or max(1024, 64 * n)
-        while True:
-            out = np.empty(cap, DET_DTYPE)
-            counts = np.zeros(n, np.int32)
-            total = C.c_int64(0)
-            rc = lib.bl_detect(self._h, _addr(a), pix, n, w, h, w, w * h, out.ctypes.data, cap,
-                               counts.ctypes.data, C.byref(total))
-            if rc == BL_ERR_CAPACITY and total.value > cap:
-                cap = int(total.value)
-                continue
-            _err(rc, total.value)
-            break
+    def _split(self, out, counts, lm, flat):
+        if flat:
+            return (out, counts, lm) if lm is not None else (out, counts)
         offs = np.concatenate([[0], np.cumsum(counts)])
-        return [out[offs[i]:offs[i + 1]].copy() for i in range(n)]
+        n = len(counts)
+        dets = [out[offs[i]:offs[i + 1]] for i in range(n)]
+        if lm is None:
+            return dets
+        return dets, [lm[offs[i]:offs[i + 1]] for i in range(n)]
 
-    def detect_landmarks(self, frames, cap=None):
-        """Detect, then landmark every kept detection -> (dets per frame, landmarks per frame)."""
+    def _sync_call(self, frames, landmarks, cap, flat):
         a, pix, n, h, w = _frames(frames)
         cap = cap or max(1024, 64 * n)
         while True:
             out = np.empty(cap, DET_DTYPE)
-            lm = np.empty((cap, self.ert_L or 1, 2))
+            lm = np.empty((cap, self.ert_L or 1, 2)) if landmarks else None
             counts = np.zeros(n, np.int32)
             total = C.c_int64(0)
-            rc = lib.bl_detect_landmarks(self._h, _addr(a), pix, n, w, h, w, w * h, out.ctypes.data, cap,
-                                         counts.ctypes.data, C.byref(total), lm.ctypes.data)
+            if landmarks:
+                rc = lib.bl_detect_landmarks(self._h, _addr(a), pix, n, w, h, w, w * h, out.ctypes.data, cap,
+                                             counts.ctypes.data, C.byref(total), lm.ctypes.data)
+            else:
+                rc = lib.bl_detect(self._h, _addr(a), pix, n, w, h, w, w * h, out.ctypes.data, cap,
+                                   counts.ctypes.data, C.byref(total))
             if rc == BL_ERR_CAPACITY and total.value > cap:
                 cap = int(total.value)
                 continue
             _err(rc, total.value)
             break
-        offs = np.concatenate([[0], np.cumsum(counts)])
-        return ([out[offs[i]:offs[i + 1]].copy() for i in range(n)],
-                [lm[offs[i]:offs[i + 1]].copy() for i in range(n)])
+        t = int(total.value)
+        return self._split(out[:t], counts, lm[:t] if lm is not None else None, flat)
+
+    def detect(self, frames, cap=None, flat=False):
+        """detect_faces over a batch -> list of DET_DTYPE arrays (one per frame), or with
+        flat=True (detections of all frames back to back, per-frame counts)."""
+        return self._sync_call(frames, False, cap, flat)
+
+    def detect_landmarks(self, frames, cap=None, flat=False):
+        """Detect, then landmark every kept detection -> (dets per frame, landmarks per frame),
+        or with flat=True (dets, counts, landmarks) back to back."""
+        return self._sync_call(frames, True, cap, flat)
+
+    # pipelined mode: up to two batches in flight (H2D / result copies overlap compute)
+    def submit(self, frames, landmarks=True):
+        a, pix, n, h, w = _frames(frames)
+        t = C.c_uint64(0)
+        _err(lib.bl_submit(self._h, _addr(a), pix, n, w, h, w, w * h, int(landmarks), C.byref(t)))
+        self._inflight[t.value] = (a, n, landmarks)  # keep the frames alive until collected
+        return t.value
+
+    def collect(self, ticket, flat=True, cap=None):
+        if ticket not in self._inflight:
+            raise RuntimeError("blinkline_b200: unknown or collected ticket")
+        a, n, landmarks = self._inflight[ticket]
+        cap = cap or max(1024, 64 * n)
+        while True:
+            out = np.empty(cap, DET_DTYPE)
+            lm = np.empty((cap, self.ert_L or 1, 2)) if landmarks else None
+            counts = np.zeros(n, np.int32)
+            total = C.c_int64(0)
+            rc = lib.bl_collect(self._h, ticket, out.ctypes.data, cap, counts.ctypes.data, C.byref(total),
+                                lm.ctypes.data if lm is not None else None)
+            if rc == BL_ERR_CAPACITY and total.value > cap:
+                cap = int(total.value)  # results stay on the device; collect again
+                continue
+            del self._inflight[ticket]
+            _err(rc, total.value)
+            break
+        t = int(total.value)
+        return self._split(out[:t], counts, lm[:t] if lm is not None else None, flat)
+
+    def set_face_capacity(self, faces_per_frame):
+        _err(lib.bl_ctx_set_face_capacity(self._h, int(faces_per_frame)))
 
     def landmarks(self, frames, frame_of_box, boxes, want_leaves=False):
         """predict_landmarks for (frame, box) pairs -> (n_boxes, L, 2) [, leaf idx (n_boxes, T*K)]."""

@@ -137,7 +137,23 @@ struct Plan {
   long long f32_elems = 0;
   long long gkeys_pf = 0;
   DevBuf arena, fmag, fori, bins, energy, feat64, feat32, cand, n_cand, dets, det_count, kept, kept_count, gkeys,
-      overflow, offsets, flat, face_frame, n_faces, input;
+      overflow, offsets;
+};
+
+// One in-flight batch: its staged input, its device results and pinned host mirrors.  Two
+// slots let batch i+1's H2D and batch i's result copies overlap compute (bl_submit/collect).
+struct Slot {
+  DevBuf input, flat, face_frame, meta, ert_out;
+  int* h_meta = nullptr;
+  size_t h_meta_cap = 0;
+  void* h_stage = nullptr;
+  size_t h_stage_cap = 0;
+  cudaEvent_t ev_h2d = nullptr, ev_done = nullptr, ev_meta = nullptr, ev_out = nullptr;
+  cudaStream_t d2h = nullptr;  // this slot's result copies: never queued behind the other slot
+  bool busy = false;
+  int n = 0, w = 0, h = 0, pix = 0, landmarks = 0;
+  long long cap_faces = 0;
+  uint64_t ticket = 0;
 };
 
 }  // namespace
@@ -163,6 +179,10 @@ struct bl_ctx {
   float stage_ms[BL_STAGE_COUNT] = {};
   int stage_launch[BL_STAGE_COUNT] = {};
   bool graphs = true;
+  cudaStream_t hst = nullptr;  // H2D stream (input frames): never queued behind a D2H wait
+  Slot slots[2];
+  uint64_t next_ticket = 1;
+  int face_cap_per_frame = 64;  // device-side capacity of landmarked faces per frame
 };
 
 namespace {
@@ -323,9 +343,6 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
   TRY(P.overflow.ensure(sizeof(int)));
   if (P.gkeys_pf) TRY(P.gkeys.ensure(nms_key_bytes() * n * P.gkeys_pf));
   TRY(P.offsets.ensure(sizeof(int) * (n + 1)));
-  TRY(P.flat.ensure(sizeof(DevDet) * n * P.cap_pf));
-  TRY(P.face_frame.ensure(sizeof(int) * n * P.cap_pf));
-  TRY(P.n_faces.ensure(sizeof(int)));
   CK(cudaMemcpy(P.desc.p, &P.host, sizeof(PlanDesc), cudaMemcpyHostToDevice));
   P.valid = true;
   return BL_OK;
@@ -396,8 +413,6 @@ int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long lon
   stage_mark(c, BL_STAGE_NMS);
   launch_nms(L, P.dets.as<DevDet>(), P.det_count.as<int>(), P.cap_pf, n, 0.5, P.kept.as<DevDet>(),
              P.kept_count.as<int>(), P.gkeys.p, P.gkeys_pf);
-  launch_flatten(L, P.kept.as<DevDet>(), P.kept_count.as<int>(), P.cap_pf, n, P.offsets.as<int>(),
-                 P.flat.as<DevDet>(), P.face_frame.as<int>(), P.n_faces.as<int>(), (long long)n * P.cap_pf);
   (void)l0;
   (void)total_out;
   return BL_OK;
@@ -451,14 +466,12 @@ int check_frames(const void* frames, int pix, int n, int w, int h, size_t pitch,
 // device; n_faces_dev holds the count.  Output landmarks -> c->ert_out.
 int run_ert(bl_ctx* c, const void* frames, int pix, int w, int h, long long pitch, long long fstride,
             const int* face_frame, const int* boxes, int box_stride, const int* n_faces_dev, int nf,
-            uint8_t* leaf_dev) {
+            uint8_t* leaf_dev, double* out_xy, int* err_dev) {
   ErtState& E = c->ert;
   const Launch L = launch_of(c);
   const int L2 = 2 * E.dev.L;
   TRY(c->ert_cur.ensure(sizeof(double) * L2 * std::max(1, nf)));
-  TRY(c->ert_out.ensure(sizeof(double) * L2 * std::max(1, nf)));
   TRY(c->ert_tf.ensure(sizeof(double2) * std::max(1, nf)));
-  TRY(c->ert_err.ensure(sizeof(int)));
   // leaf indices: the caller's [face][T*K] buffer, else a per-level scratch [face][K]
   long long leaf_stride = (long long)E.dev.T * E.dev.K;
   uint8_t* leaf = leaf_dev;
@@ -467,14 +480,13 @@ int run_ert(bl_ctx* c, const void* frames, int pix, int w, int h, long long pitc
     TRY(c->ert_leafs.ensure((size_t)std::max(1, nf) * leaf_stride + 16));
     leaf = c->ert_leafs.as<uint8_t>();
   }
-  CK(cudaMemsetAsync(c->ert_err.p, 0, sizeof(int), c->st));
+  CK(cudaMemsetAsync(err_dev, 0, sizeof(int), c->st));
   launch_ert_init(L, E.dev, n_faces_dev, nf, c->ert_cur.as<double>());
   for (int t = 0; t < E.dev.T; ++t)
     launch_ert_level(L, E.dev, t, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
                      n_faces_dev, nf, c->ert_cur.as<double>(), c->ert_tf.as<double2>(),
-                     leaf_dev ? leaf + (long long)t * E.dev.K : leaf, leaf_stride, c->ert_err.as<int>());
-  launch_ert_finish(L, E.dev, boxes, box_stride, n_faces_dev, nf, c->ert_cur.as<double>(),
-                    c->ert_out.as<double>());
+                     leaf_dev ? leaf + (long long)t * E.dev.K : leaf, leaf_stride, err_dev);
+  launch_ert_finish(L, E.dev, boxes, box_stride, n_faces_dev, nf, c->ert_cur.as<double>(), out_xy);
   return BL_OK;
 }
 
@@ -498,6 +510,146 @@ void timing_end(bl_ctx* c, const int* present, int n_present) {
   }
 }
 
+int ensure_pinned(void*& p, size_t& cap, size_t bytes) {
+  if (cap >= bytes && p) return BL_OK;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  cap = 0;
+  CK(cudaMallocHost(&p, std::max<size_t>(bytes, 4096)));
+  cap = std::max<size_t>(bytes, 4096);
+  return BL_OK;
+}
+
+bool is_pinned_or_device(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Enqueues detect (+ landmarks) for one batch into slot `s`: no host synchronisation.
+int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, size_t pitch, size_t fstride,
+            int landmarks) {
+  Slot& S = c->slots[s];
+  Plan& P = c->plan;
+  const DetectorState& D = c->det;
+  const bool same = P.valid && P.n == n && P.w == w && P.h == h && P.pix == pix &&
+                    P.window_cells == D.window_cells && P.cell_px == D.cell_px;
+  if (!same) {  // arenas may be reallocated: nothing may still be reading them
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaStreamSynchronize(c->hst));
+    for (Slot& o : c->slots) CK(cudaStreamSynchronize(o.d2h));
+  }
+  timing_begin(c);
+  const void* dev = nullptr;
+  long long dp = 0, df = 0;
+  const size_t es = pix == BL_PIX_U8 ? 1 : 8;
+  if (is_device_ptr(frames)) {
+    dev = frames;
+    dp = (long long)pitch;
+    df = (long long)fstride;
+  } else {  // H2D on the copy stream, after the slot's previous batch stopped reading its input
+    TRY(S.input.ensure(es * (size_t)n * w * h));
+    CK(cudaStreamWaitEvent(c->hst, S.ev_done, 0));
+    if (pitch == (size_t)w && fstride == (size_t)w * h) {
+      CK(cudaMemcpyAsync(S.input.p, frames, es * (size_t)n * w * h, cudaMemcpyDefault, c->hst));
+    } else {
+      for (int i = 0; i < n; ++i)
+        CK(cudaMemcpy2DAsync((char*)S.input.p + es * (size_t)i * w * h, es * w,
+                             (const char*)frames + es * fstride * i, es * pitch, es * w, h, cudaMemcpyDefault,
+                             c->hst));
+    }
+    CK(cudaEventRecord(S.ev_h2d, c->hst));
+    CK(cudaStreamWaitEvent(c->st, S.ev_h2d, 0));
+    dev = S.input.p;
+    dp = w;
+    df = (long long)w * h;
+  }
+  TRY(run_detect(c, dev, pix, n, w, h, dp, df, nullptr));
+  const long long cap_faces = std::max<long long>(1, (long long)n * c->face_cap_per_frame);
+  TRY(S.flat.ensure(sizeof(DevDet) * cap_faces));
+  TRY(S.face_frame.ensure(sizeof(int) * cap_faces));
+  TRY(S.meta.ensure(sizeof(int) * (n + 4)));
+  int* meta = S.meta.as<int>();
+  launch_flatten(launch_of(c), P.kept.as<DevDet>(), P.kept_count.as<int>(), P.cap_pf, n, P.offsets.as<int>(),
+                 S.flat.as<DevDet>(), S.face_frame.as<int>(), meta, cap_faces, P.overflow.as<int>());
+  if (landmarks) {
+    TRY(S.ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * cap_faces));
+    stage_mark(c, BL_STAGE_ERT);
+    TRY(run_ert(c, dev, pix, w, h, dp, df, S.face_frame.as<int>(), S.flat.as<int>(), 8, meta + n, (int)cap_faces,
+                nullptr, S.ert_out.as<double>(), meta + n + 2));
+  } else {
+    CK(cudaMemsetAsync(meta + n + 2, 0, sizeof(int), c->st));
+  }
+  CK(cudaEventRecord(S.ev_done, c->st));
+  // counts + flags back on the slot's D2H stream as soon as compute finishes
+  TRY(ensure_pinned(reinterpret_cast<void*&>(S.h_meta), S.h_meta_cap, sizeof(int) * (n + 4)));
+  CK(cudaStreamWaitEvent(S.d2h, S.ev_done, 0));
+  CK(cudaMemcpyAsync(S.h_meta, meta, sizeof(int) * (n + 3), cudaMemcpyDeviceToHost, S.d2h));
+  CK(cudaEventRecord(S.ev_meta, S.d2h));
+  S.busy = true;
+  S.n = n;
+  S.w = w;
+  S.h = h;
+  S.pix = pix;
+  S.landmarks = landmarks;
+  S.cap_faces = cap_faces;
+  return BL_OK;
+}
+
+// Waits for slot `s` and copies its results out.  On BL_ERR_CAPACITY for the caller's output
+// buffer the slot stays busy (results remain on the device; collect again with more room).
+int collect(bl_ctx* c, int s, bl_detection* out, int64_t cap, int32_t* counts, int64_t* total, double* landmarks) {
+  Slot& S = c->slots[s];
+  if (!S.busy) return set_err(BL_ERR_STATE, "nothing submitted in this slot");
+  CK(cudaEventSynchronize(S.ev_meta));
+  CK(cudaGetLastError());
+  const int n = S.n;
+  const int* m = S.h_meta;
+  if (m[n + 1]) {
+    S.busy = false;
+    return set_err(BL_ERR_CAPACITY, "raw detection capacity exceeded");
+  }
+  const int64_t tot = m[n];
+  if (total) *total = tot;
+  if (counts) std::memcpy(counts, m, sizeof(int32_t) * n);
+  if (S.landmarks && m[n + 2] == 1) {
+    S.busy = false;
+    return set_err(BL_ERR_INVALID, "similarity_transform: source shape has no spread");
+  }
+  if (S.landmarks && m[n + 2] == 2) {
+    S.busy = false;
+    return set_err(BL_ERR_INVALID, "similarity_transform: target shape has no spread");
+  }
+  if (tot > S.cap_faces) {
+    S.busy = false;
+    return set_err(BL_ERR_CAPACITY, "%lld kept detections exceed the device face capacity %lld "
+                   "(bl_ctx_set_face_capacity)", (long long)tot, (long long)S.cap_faces);
+  }
+  if (tot > cap)
+    return set_err(BL_ERR_CAPACITY, "output capacity %lld < %lld detections", (long long)cap, (long long)tot);
+  stage_mark(c, BL_STAGE_D2H);
+  const size_t bd = sizeof(bl_detection) * tot;
+  const size_t bl = S.landmarks && landmarks ? sizeof(double) * 2 * c->ert.dev.L * tot : 0;
+  const bool direct_d = !out || is_pinned_or_device(out);
+  const bool direct_l = !bl || is_pinned_or_device(landmarks);
+  TRY(ensure_pinned(S.h_stage, S.h_stage_cap, (direct_d ? 0 : bd) + (direct_l ? 0 : bl) + 64));
+  char* stage = static_cast<char*>(S.h_stage);
+  if (tot > 0 && out)
+    CK(cudaMemcpyAsync(direct_d ? (void*)out : stage, S.flat.p, bd, cudaMemcpyDefault, S.d2h));
+  if (bl)
+    CK(cudaMemcpyAsync(direct_l ? (void*)landmarks : stage + (direct_d ? 0 : bd), S.ert_out.p, bl, cudaMemcpyDefault,
+                       S.d2h));
+  CK(cudaEventRecord(S.ev_out, S.d2h));
+  CK(cudaEventSynchronize(S.ev_out));
+  if (tot > 0 && out && !direct_d) std::memcpy(out, stage, bd);
+  if (bl && !direct_l) std::memcpy(landmarks, stage + (direct_d ? 0 : bd), bl);
+  S.busy = false;
+  return BL_OK;
+}
+
 int detect_common(bl_ctx* c, const void* frames, int pix, int n, int w, int h, size_t pitch, size_t fstride,
                   bl_detection* out, int64_t cap, int32_t* counts, int64_t* total, double* landmarks) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
@@ -511,54 +663,33 @@ int detect_common(bl_ctx* c, const void* frames, int pix, int n, int w, int h, s
     if (total) *total = 0;
     return BL_OK;
   }
-  timing_begin(c);
-  const void* dev = nullptr;
-  long long dp = 0, df = 0;
-  TRY(stage_input(c, c->plan.input, frames, pix, n, w, h, pitch, fstride, &dev, &dp, &df));
-  TRY(run_detect(c, dev, pix, n, w, h, dp, df, nullptr));
-  Plan& P = c->plan;
-  TRY(ensure_counts(c, n + 2));
-  CK(cudaMemcpyAsync(c->h_counts, P.kept_count.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(c->h_counts + n, P.overflow.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  CK(cudaGetLastError());
-  if (c->h_counts[n]) return set_err(BL_ERR_CAPACITY, "raw detection capacity exceeded");
-  int64_t tot = 0;
-  for (int i = 0; i < n; ++i) {
-    if (counts) counts[i] = c->h_counts[i];
-    tot += c->h_counts[i];
-  }
-  if (total) *total = tot;
-  if (tot > cap) return set_err(BL_ERR_CAPACITY, "output capacity %lld < %lld detections", (long long)cap,
-                                (long long)tot);
-  if (landmarks && tot > 0) {
-    stage_mark(c, BL_STAGE_ERT);
-    TRY(run_ert(c, dev, pix, w, h, dp, df, P.face_frame.as<int>(), P.flat.as<int>(), 8, P.n_faces.as<int>(),
-                (int)tot, nullptr));
-  }
-  stage_mark(c, BL_STAGE_D2H);
-  if (tot > 0 && out)
-    CK(cudaMemcpyAsync(out, P.flat.p, sizeof(bl_detection) * tot, cudaMemcpyDefault, c->st));
-  if (landmarks && tot > 0)
-    CK(cudaMemcpyAsync(landmarks, c->ert_out.p, sizeof(double) * 2 * c->ert.dev.L * tot, cudaMemcpyDefault,
-                       c->st));
-  CK(cudaStreamSynchronize(c->st));
-  CK(cudaGetLastError());
-  if (landmarks && tot > 0) {
-    int err = 0;
-    CK(cudaMemcpy(&err, c->ert_err.p, sizeof(int), cudaMemcpyDeviceToHost));
-    if (err == 1) return set_err(BL_ERR_INVALID, "similarity_transform: source shape has no spread");
-    if (err == 2) return set_err(BL_ERR_INVALID, "similarity_transform: target shape has no spread");
+  for (int s = 0; s < 2; ++s)
+    if (c->slots[s].busy) return set_err(BL_ERR_STATE, "submitted batches must be collected first");
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    TRY(enqueue(c, 0, frames, pix, n, w, h, pitch, fstride, landmarks != nullptr));
+    int64_t tot = 0;
+    const int rc = collect(c, 0, out, cap, counts, &tot, landmarks);
+    if (total) *total = tot;
+    if (rc == BL_ERR_CAPACITY && tot > c->slots[0].cap_faces && attempt == 0) {
+      // more kept detections than the device face capacity: grow it and redo the batch
+      c->face_cap_per_frame = (int)std::max<long long>(c->face_cap_per_frame, div_up(tot, n) + 1);
+      if (tot > (long long)n * c->face_cap_per_frame) c->face_cap_per_frame = (int)div_up(tot, n) + 1;
+      continue;
+    }
+    if (rc != BL_OK) {
+      c->slots[0].busy = false;
+      return rc;
+    }
+    break;
   }
   const int present_det[] = {BL_STAGE_H2D, BL_STAGE_PYRAMID, BL_STAGE_GRADHIST, BL_STAGE_FEATURES,
                              BL_STAGE_SCREEN, BL_STAGE_RESCORE, BL_STAGE_NMS, BL_STAGE_ERT, BL_STAGE_D2H};
-  if (landmarks && tot > 0) {
+  const int p2[] = {BL_STAGE_H2D, BL_STAGE_PYRAMID, BL_STAGE_GRADHIST, BL_STAGE_FEATURES,
+                    BL_STAGE_SCREEN, BL_STAGE_RESCORE, BL_STAGE_NMS, BL_STAGE_D2H};
+  if (landmarks)
     timing_end(c, present_det, 9);
-  } else {
-    const int p2[] = {BL_STAGE_H2D, BL_STAGE_PYRAMID, BL_STAGE_GRADHIST, BL_STAGE_FEATURES,
-                      BL_STAGE_SCREEN, BL_STAGE_RESCORE, BL_STAGE_NMS, BL_STAGE_D2H};
+  else
     timing_end(c, p2, 8);
-  }
   return BL_OK;
 }
 
@@ -669,7 +800,15 @@ int bl_ctx_create(int device, bl_ctx** out) {
   auto c = std::make_unique<bl_ctx>();
   c->device = device;
   CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->hst, cudaStreamNonBlocking));
   c->st = c->own;
+  for (Slot& S : c->slots) {
+    CK(cudaStreamCreateWithFlags(&S.d2h, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&S.ev_h2d, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&S.ev_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&S.ev_meta, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&S.ev_out, cudaEventDisableTiming));
+  }
   for (auto& e : c->ev) CK(cudaEventCreate(&e));
   // hog.cpp:12-24: the 18 directions from the host libm, exactly as the reference builds them
   double ux[kBins], uy[kBins];
@@ -688,12 +827,25 @@ void bl_ctx_destroy(bl_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
+  if (c->hst) cudaStreamSynchronize(c->hst);
   if (c->h_counts) cudaFreeHost(c->h_counts);
+  for (Slot& S : c->slots) {
+    if (S.h_meta) cudaFreeHost(S.h_meta);
+    if (S.h_stage) cudaFreeHost(S.h_stage);
+    for (cudaEvent_t e : {S.ev_h2d, S.ev_done, S.ev_meta, S.ev_out})
+      if (e) cudaEventDestroy(e);
+    if (S.d2h) {
+      cudaStreamSynchronize(S.d2h);
+      cudaStreamDestroy(S.d2h);
+    }
+  }
+  cudaStream_t hst = c->hst;
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t own = c->own;
   delete c;  // DevBufs free on their device
   if (own) cudaStreamDestroy(own);
+  if (hst) cudaStreamDestroy(hst);
 }
 
 int bl_ctx_set_stream(bl_ctx* c, void* stream) {
@@ -872,6 +1024,43 @@ int bl_detect_landmarks(bl_ctx* c, const void* frames, int pixel_type, int n, in
   return detect_common(c, frames, pixel_type, n, w, h, pitch, frame_stride, out, cap, counts, total, landmarks);
 }
 
+int bl_ctx_set_face_capacity(bl_ctx* c, int faces_per_frame) {
+  if (!c || faces_per_frame < 1) return set_err(BL_ERR_INVALID, "bad face capacity");
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->face_cap_per_frame = faces_per_frame;
+  return BL_OK;
+}
+
+int bl_submit(bl_ctx* c, const void* frames, int pixel_type, int n, int w, int h, size_t pitch, size_t frame_stride,
+              int with_landmarks, uint64_t* ticket) {
+  if (!c || !ticket) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->det.ready) return set_err(BL_ERR_STATE, "no detector model uploaded");
+  if (with_landmarks && !c->ert.ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
+  if (frame_stride == 0) frame_stride = pitch * h;
+  TRY(check_frames(frames, pixel_type, n, w, h, pitch, frame_stride));
+  if (n < 1) return set_err(BL_ERR_INVALID, "empty batch");
+  TRY(use_device(c));
+  const uint64_t t = c->next_ticket;
+  const int s = (int)(t & 1);
+  if (c->slots[s].busy) return set_err(BL_ERR_STATE, "two batches in flight: collect one before submitting");
+  TRY(enqueue(c, s, frames, pixel_type, n, w, h, pitch, frame_stride, with_landmarks != 0));
+  c->slots[s].ticket = t;
+  c->next_ticket = t + 1;
+  *ticket = t;
+  return BL_OK;
+}
+
+int bl_collect(bl_ctx* c, uint64_t ticket, bl_detection* out, int64_t cap, int32_t* counts, int64_t* total,
+               double* landmarks) {
+  if (!c) return set_err(BL_ERR_INVALID, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  const int s = (int)(ticket & 1);
+  if (!c->slots[s].busy || c->slots[s].ticket != ticket) return set_err(BL_ERR_STATE, "unknown or collected ticket");
+  TRY(use_device(c));
+  return collect(c, s, out, cap, counts, total, landmarks);
+}
+
 int bl_landmarks(bl_ctx* c, const void* frames, int pixel_type, int n_frames, int w, int h, size_t pitch,
                  size_t frame_stride, const int32_t* frame_of_box, const bl_box* boxes, int64_t n_boxes,
                  double* out_xy, uint8_t* leaf_idx) {
@@ -910,8 +1099,10 @@ int bl_landmarks(bl_ctx* c, const void* frames, int pixel_type, int n_frames, in
     leaf_dev = c->ert_leaf.as<uint8_t>();
   }
   stage_mark(c, BL_STAGE_ERT);
+  TRY(c->ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * std::max(1, nf)));
+  TRY(c->ert_err.ensure(sizeof(int)));
   TRY(run_ert(c, dev, pixel_type, w, h, dp, df, c->ert_frames.as<int>(), c->ert_boxes.as<int>(), 4,
-              c->ert_nfaces.as<int>(), nf, leaf_dev));
+              c->ert_nfaces.as<int>(), nf, leaf_dev, c->ert_out.as<double>(), c->ert_err.as<int>()));
   stage_mark(c, BL_STAGE_D2H);
   CK(cudaMemcpyAsync(out_xy, c->ert_out.p, sizeof(double) * 2 * c->ert.dev.L * n_boxes, cudaMemcpyDefault, c->st));
   if (leaf_idx)

@@ -255,7 +255,9 @@ __global__ void __launch_bounds__(1024) k_flatten(const DevDet* __restrict__ kep
                                                   const int* __restrict__ kept_count, long long cap_pf,
                                                   int n_frames, int* __restrict__ offsets,
                                                   DevDet* __restrict__ flat, int* __restrict__ face_frame,
-                                                  int* __restrict__ n_faces, long long flat_cap) {
+                                                  int* __restrict__ meta, long long flat_cap,
+                                                  const int* __restrict__ raw_overflow) {
+  // meta: [0, n) kept count per frame, [n] total kept, [n+1] raw-detection overflow flag
   __shared__ int s_part[1024];
   const int tid = threadIdx.x;
   // each thread scans a contiguous chunk of frames
@@ -274,11 +276,13 @@ __global__ void __launch_bounds__(1024) k_flatten(const DevDet* __restrict__ kep
   int run = s_part[tid] - sum;
   for (int f = f0; f < f1; ++f) {
     offsets[f] = run;
+    meta[f] = kept_count[f];
     run += kept_count[f];
   }
   if (tid == blockDim.x - 1) {
     offsets[n_frames] = s_part[tid];
-    *n_faces = s_part[tid];
+    meta[n_frames] = s_part[tid];
+    meta[n_frames + 1] = *raw_overflow;
   }
   __syncthreads();
   // copy: warp per frame
@@ -296,10 +300,10 @@ __global__ void __launch_bounds__(1024) k_flatten(const DevDet* __restrict__ kep
 }
 
 void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, long long cap_pf,
-                    int n_frames, int* offsets, DevDet* flat, int* face_frame, int* n_faces,
-                    long long flat_cap) {
-  k_flatten<<<1, 1024, 0, L.st>>>(kept, kept_count, cap_pf, n_frames, offsets, flat, face_frame, n_faces,
-                                  flat_cap);
+                    int n_frames, int* offsets, DevDet* flat, int* face_frame, int* meta,
+                    long long flat_cap, const int* raw_overflow) {
+  k_flatten<<<1, 1024, 0, L.st>>>(kept, kept_count, cap_pf, n_frames, offsets, flat, face_frame, meta,
+                                  flat_cap, raw_overflow);
   ++*L.counter;
 }
 

@@ -171,8 +171,8 @@ long long nms_gkeys_per_frame(long long cap_pf);
 void launch_nms(const Launch& L, const DevDet* dets, const int* det_count, long long cap_pf, int n_frames,
                 double iou_thr, DevDet* kept_out, int* kept_count, void* gkeys, long long gkeys_pf);
 void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, long long cap_pf,
-                    int n_frames, int* offsets, DevDet* flat, int* face_frame, int* n_faces,
-                    long long flat_cap);
+                    int n_frames, int* offsets, DevDet* flat, int* face_frame, int* meta,
+                    long long flat_cap, const int* raw_overflow);
 // bl_ert.cu
 void launch_ert_init(const Launch& L, const ErtDev& M, const int* n_faces, int cap, double* cur);
 void launch_ert_level(const Launch& L, const ErtDev& M, int t, const void* frames, int u8, int w, int h,

@@ -394,3 +394,47 @@ def test_device_resident_frames_and_launch_count(ctx, pattern_model):
     assert ctx.launch_count > before
     for a, b in zip(host, dev):
         assert np.array_equal(a, b)
+
+
+# --------------------------------------------------------------- pipelined mode ----
+def test_submit_collect_matches_sync(ctx, pattern_model):
+    from pyoracle import random_ert, ring_frames_np
+    ctx.upload_detector(pattern_model)
+    ctx.upload_ert(random_ert(T=2, K=20, F=3, seed=9))
+    a = ring_frames_np(5, 320, 240, seed=21)
+    b = ring_frames_np(5, 320, 240, seed=22)
+    sa = ctx.detect_landmarks(a, flat=True)
+    sb = ctx.detect_landmarks(b, flat=True)
+    ta = ctx.submit(a)
+    tb = ctx.submit(b)  # two in flight
+    with pytest.raises(RuntimeError):
+        ctx.submit(a)  # a third would reuse a busy slot
+    ra = ctx.collect(ta)
+    tc = ctx.submit(b)
+    rb = ctx.collect(tb)
+    rc = ctx.collect(tc)
+    for got, want in [(ra, sa), (rb, sb), (rc, sb)]:
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+        assert np.array_equal(got[2], want[2])
+    with pytest.raises(RuntimeError):
+        ctx.collect(ta)  # already collected
+
+
+def test_face_capacity_overflow(ctx):
+    """More kept detections than the device face capacity: collect reports it, the synchronous
+    call grows the capacity and still returns every detection with landmarks."""
+    import paper_2006_00816_b200 as bl
+    from pyoracle import random_ert
+    r = rng(78)
+    model = {"weights": r.uniform(-1, 1, (5, 3100)) * 0.05, "biases": r.uniform(-1, 1, 5), "threshold": 0.3}
+    img = np.floor(r.uniform(0, 256, (1, 240, 320))).astype(np.uint8)
+    ctx.upload_detector(model)
+    ctx.upload_ert(random_ert(T=1, K=4, F=2, seed=1))
+    ctx.set_face_capacity(2)
+    t = ctx.submit(img)
+    with pytest.raises(bl.CapacityError):
+        ctx.collect(t)
+    dets, counts, lms = ctx.detect_landmarks(img, flat=True)
+    assert len(dets) == counts.sum() > 2 and lms.shape[0] == len(dets)
+    assert np.array_equal(dets, ctx.detect(img, flat=True)[0])
+    ctx.set_face_capacity(64)
