@@ -6,10 +6,11 @@ import sys
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
 hdr = rows[0]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
+mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
 agg = collections.OrderedDict()
 for r in rows[1:]:
-    if r[ki] == "Kernel Name":
+    if r[ki] == "Kernel Name" or (mi is not None and r[mi] != "gpu__time_duration.sum"):
         continue
     name = r[ki].split("(")[0].replace("void ", "")
     agg.setdefault(name, []).append(float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0))
