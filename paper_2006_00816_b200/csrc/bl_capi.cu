@@ -128,6 +128,7 @@ struct Plan {
   int n_levels = 0;
   std::vector<int> lw, lh;
   std::vector<long long> arena_off;  // levels >= 1, in doubles
+  std::vector<int> lpitch;           // levels >= 1: row pitch in doubles (multiple of 4)
   long long arena_elems = 0;
   std::vector<int> scored;           // pyramid level of each scored slot
   PlanDesc host{};
@@ -136,7 +137,7 @@ struct Plan {
   long long cand_cap = 0;
   long long f32_elems = 0;
   long long gkeys_pf = 0;
-  DevBuf arena, fmag, fori, bins, energy, feat64, feat32, cand, n_cand, dets, det_count, kept, kept_count, gkeys,
+  DevBuf arena, bins, energy, feat64, feat32, cand, n_cand, dets, det_count, kept, kept_count, gkeys,
       overflow, offsets;
 };
 
@@ -230,10 +231,12 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
   P.n_levels = (int)P.lw.size();
   if (P.n_levels > kMaxLevels) return set_err(BL_ERR_INVALID, "pyramid deeper than %d levels", kMaxLevels);
   P.arena_off.assign(P.n_levels, 0);
+  P.lpitch.assign(P.n_levels, 0);
   long long off = 0;
   for (int k = 1; k < P.n_levels; ++k) {
+    P.lpitch[k] = (int)div_up(P.lw[k], 4) * 4;  // 32-B aligned rows: 16-B vector loads in k_hog
     P.arena_off[k] = off;
-    off += (long long)n * P.lw[k] * P.lh[k];
+    off += (long long)n * P.lpitch[k] * P.lh[k];
   }
   P.arena_elems = off;
 
@@ -272,8 +275,8 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
       L.pix_pitch = 0;
     } else {
       L.pix_off = P.arena_off[k];
-      L.pix_fstride = (long long)L.w * L.h;
-      L.pix_pitch = L.w;
+      L.pix_fstride = (long long)P.lpitch[k] * L.h;
+      L.pix_pitch = P.lpitch[k];
     }
     L.cell_off = cells;
     L.cell_begin = cells;
@@ -325,8 +328,6 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
 
   TRY(P.desc.ensure(sizeof(PlanDesc)));
   TRY(P.arena.ensure(sizeof(double) * std::max<long long>(1, P.arena_elems)));
-  TRY(P.fmag.ensure(sizeof(double) * std::max<long long>(1, fld)));
-  TRY(P.fori.ensure(std::max<long long>(1, fld)));
   TRY(P.bins.ensure(sizeof(double) * kBins * std::max<long long>(1, cells)));
   TRY(P.energy.ensure(sizeof(double) * std::max<long long>(1, cells)));
   TRY(P.feat64.ensure(sizeof(double) * kFeat * std::max<long long>(1, cells)));
@@ -379,10 +380,10 @@ int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long lon
   for (int k = 1; k < P.n_levels; ++k) {
     const void* src = k == 1 ? in : (const void*)(P.arena.as<double>() + P.arena_off[k - 1]);
     const int src_u8 = (k == 1 && pix == BL_PIX_U8);
-    const long long sp = k == 1 ? pitch : P.lw[k - 1];
-    const long long sf = k == 1 ? fstride : (long long)P.lw[k - 1] * P.lh[k - 1];
+    const long long sp = k == 1 ? pitch : P.lpitch[k - 1];
+    const long long sf = k == 1 ? fstride : (long long)P.lpitch[k - 1] * P.lh[k - 1];
     launch_resample(L, src, src_u8, P.lw[k - 1], P.lh[k - 1], sp, sf, P.arena.as<double>() + P.arena_off[k],
-                    P.lw[k], P.lh[k], (long long)P.lw[k] * P.lh[k], n);
+                    P.lw[k], P.lh[k], P.lpitch[k], (long long)P.lpitch[k] * P.lh[k], n);
   }
   stage_mark(c, BL_STAGE_GRADHIST);
   const PlanDesc* Pd = P.desc.as<PlanDesc>();
@@ -391,14 +392,13 @@ int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long lon
   CK(cudaMemsetAsync(P.det_count.p, 0, sizeof(int) * n, c->st));
   CK(cudaMemsetAsync(P.overflow.p, 0, sizeof(int), c->st));
   if (ns > 0) {
+    // fused gradient + histogram + energy (the gradient field stays on chip)
     int s1 = 0;
     if (P.scored[0] == 0) {  // level 0 reads the caller's frames (u8 or f64)
-      launch_grad(L, P.host, Pd, 0, 1, in, pix == BL_PIX_U8 ? 0 : 1, P.fmag.as<double>(), P.fori.as<uint8_t>());
+      launch_hog(L, P.host, Pd, 0, 1, in, pix == BL_PIX_U8 ? 0 : 1, P.bins.as<double>(), P.energy.as<double>());
       s1 = 1;
     }
-    launch_grad(L, P.host, Pd, s1, ns, P.arena.as<double>(), 1, P.fmag.as<double>(), P.fori.as<uint8_t>());
-    launch_gradhist(L, P.host, Pd, P.fmag.as<double>(), P.fori.as<uint8_t>(), P.bins.as<double>(),
-                    P.energy.as<double>());
+    launch_hog(L, P.host, Pd, s1, ns, P.arena.as<double>(), 1, P.bins.as<double>(), P.energy.as<double>());
   }
   stage_mark(c, BL_STAGE_FEATURES);
   launch_features(L, P.host, Pd, P.bins.as<double>(), P.energy.as<double>(), P.feat64.as<double>(),
@@ -1163,7 +1163,7 @@ int bl_build_pyramid(bl_ctx* c, const void* image, int pix, int w, int h, int wi
   }
   for (int k = 1; k < nl; ++k)
     launch_resample(L, lv + off[k - 1], 0, lw[k - 1], lh[k - 1], lw[k - 1], (long long)lw[k - 1] * lh[k - 1],
-                    lv + off[k], lw[k], lh[k], (long long)lw[k] * lh[k], 1);
+                    lv + off[k], lw[k], lh[k], lw[k], (long long)lw[k] * lh[k], 1);
   return from_device(c, out, lv, sizeof(double) * total);
 }
 
@@ -1176,7 +1176,7 @@ int bl_downscale_bilinear(bl_ctx* c, const double* image, int w, int h, double* 
   const void* src = nullptr;
   TRY(to_device(c, c->s_a, image, sizeof(double) * w * h, &src));
   TRY(c->s_b.ensure(sizeof(double) * dw * dh));
-  launch_resample(launch_of(c), src, 0, w, h, w, (long long)w * h, c->s_b.as<double>(), dw, dh, (long long)dw * dh, 1);
+  launch_resample(launch_of(c), src, 0, w, h, w, (long long)w * h, c->s_b.as<double>(), dw, dh, dw, (long long)dw * dh, 1);
   return from_device(c, out, c->s_b.p, sizeof(double) * dw * dh);
 }
 
@@ -1270,12 +1270,8 @@ int bl_extract_features(bl_ctx* c, const double* image, int w, int h, double* fe
   TRY(c->s_b.ensure(sizeof(double) * kBins * cells));
   TRY(c->s_c.ensure(sizeof(double) * cells));
   TRY(c->s_d.ensure(sizeof(double) * kFeat * cells));
-  TRY(c->s_e.ensure(sizeof(double) * w * h + (size_t)w * h + 16));
-  double* fm = c->s_e.as<double>();
-  uint8_t* fo = reinterpret_cast<uint8_t*>(fm + (size_t)w * h);
   const Launch L = launch_of(c);
-  launch_grad(L, H, c->s_desc.as<PlanDesc>(), 0, 1, src, 1, fm, fo);
-  launch_gradhist(L, H, c->s_desc.as<PlanDesc>(), fm, fo, c->s_b.as<double>(), c->s_c.as<double>());
+  launch_hog(L, H, c->s_desc.as<PlanDesc>(), 0, 1, src, 1, c->s_b.as<double>(), c->s_c.as<double>());
   launch_features(L, H, c->s_desc.as<PlanDesc>(), c->s_b.as<double>(), c->s_c.as<double>(), c->s_d.as<double>(),
                   nullptr);
   if (bins) CK(cudaMemcpyAsync(bins, c->s_b.p, sizeof(double) * kBins * cells, cudaMemcpyDefault, c->st));

@@ -36,7 +36,18 @@ BL_DEV double exact_window_score3(const double* __restrict__ feat, int cw, int c
 
 BL_DEV int round_half_up(double v) { return (int)floor(dadd(v, 0.5)); }  // detector.cpp:41
 
-__global__ void __launch_bounds__(256) k_rescore(const PlanDesc* __restrict__ P,
+// The re-score proper.  A warp scores three candidates; lanes 10g + j (g < 3) own window
+// row j of candidate g and run its 310-term dot product strictly in the reference's order.
+// The operands are staged one window cell (31 features) at a time into padded shared memory
+// with coalesced loads -- lane f of the warp fetches feature/weight f of each of the 30
+// (candidate, row) strips -- so global traffic is 248-B contiguous segments instead of one
+// 8-B scalar per lane per term.  Row pitch 33 doubles keeps the 30 strips on distinct banks.
+constexpr int kRsPitch = 33;
+constexpr int kRsWarps = 4;
+constexpr int kRsWarpDoubles = 2 * 30 * kRsPitch;
+constexpr size_t kRsSmem = sizeof(double) * kRsWarps * kRsWarpDoubles;  // 63,360 B
+
+__global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __restrict__ P,
                                                  const double* __restrict__ feat64,
                                                  const double* __restrict__ w64,
                                                  const double* __restrict__ bias, double thr,
@@ -45,19 +56,61 @@ __global__ void __launch_bounds__(256) k_rescore(const PlanDesc* __restrict__ P,
                                                  long long cand_cap, DevDet* __restrict__ dets,
                                                  int* __restrict__ det_count, long long cap_pf,
                                                  int* __restrict__ overflow) {
-  const int lane = threadIdx.x & 31;
+  extern __shared__ double rs_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* Fs = rs_smem + warp * kRsWarpDoubles;
+  double* Ws = Fs + 30 * kRsPitch;
   const int g = lane / 10;
   const long long n = min((long long)*n_cand, cand_cap);
-  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long i0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 3; i0 < n; i0 += nw * 3) {
+  const long long nw = (long long)gridDim.x * kRsWarps;
+  for (long long i0 = ((long long)blockIdx.x * kRsWarps + warp) * 3; i0 < n; i0 += nw * 3) {
+    // strip bases of the three candidates (row 0 of the window, cell 0): every lane holds all
+    const double* fst[3];
+    const double* wst[3];
+    int cwv[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const Candidate c = cand[min(i0 + q, n - 1)];
+      const LevelDesc& D = P->lv[c.slot_r >> 3];
+      cwv[q] = D.cw;
+      fst[q] = feat64 + (D.cell_off + (long long)c.frame * D.cw * D.ch + (long long)c.cy * D.cw + c.cx) * kFeat;
+      wst[q] = w64 + (c.slot_r & 7) * kFilterW;
+    }
+    double acc = 0.0;
+#pragma unroll 1
+    for (int ci = 0; ci < kWin; ++ci) {
+      if (lane < kFeat) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+#pragma unroll
+          for (int j = 0; j < kWin; ++j) {
+            Fs[(q * 10 + j) * kRsPitch + lane] = __ldg(fst[q] + ((long long)j * cwv[q] + ci) * kFeat + lane);
+            Ws[(q * 10 + j) * kRsPitch + lane] = __ldg(wst[q] + j * kRowW + ci * kFeat + lane);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < 30) {
+        const double* fr = Fs + lane * kRsPitch;
+        const double* wr = Ws + lane * kRsPitch;
+#pragma unroll
+        for (int f = 0; f < kFeat; ++f) acc = dadd(acc, dmul(fr[f], wr[f]));  // detector.cpp:84
+      }
+      __syncwarp();
+    }
+    // column pass (detector.cpp:91-95): the ten row sums in order, then + bias
+    const int base = (g < 3 ? g : 0) * 10;
+    double total = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < kWin; ++jj) total = dadd(total, __shfl_sync(0xffffffffu, acc, base + jj));
     const long long i = i0 + (g < 3 ? g : 0);
     const bool active = g < 3 && i < n;
-    const Candidate c = cand[active ? i : i0];
+    if (!active || lane != 10 * g) continue;
+    const Candidate c = cand[i];
     const int s = c.slot_r >> 3, r = c.slot_r & 7;
     const LevelDesc& D = P->lv[s];
-    const double* fb = feat64 + (D.cell_off + (long long)c.frame * D.cw * D.ch) * kFeat;
-    const double sc = exact_window_score3(fb, D.cw, c.cx, c.cy, w64 + r * kFilterW, bias[r], lane, active);
-    if (active && lane == 10 * g && sc > thr) {  // detector.cpp:110 (strict)
+    const double sc = dadd(total, bias[r]);
+    if (sc > thr) {  // detector.cpp:110 (strict)
       DevDet d;
       d.x = round_half_up(ddiv((double)(c.cx * cell_px), D.c));
       d.y = round_half_up(ddiv((double)(c.cy * cell_px), D.c));
@@ -79,7 +132,12 @@ void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, c
                     const double* bias, double thr, int cell_px, const Candidate* cand,
                     const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
                     int* det_count, long long cap_pf, int* overflow, int blocks) {
-  k_rescore<<<blocks, 256, 0, L.st>>>(Pd, feat64, w64, bias, thr, cell_px, cand, n_cand, cand_cap,
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRsSmem);
+    attr = true;
+  }
+  k_rescore<<<blocks, 32 * kRsWarps, kRsSmem, L.st>>>(Pd, feat64, w64, bias, thr, cell_px, cand, n_cand, cand_cap,
                                       dets, det_count, cap_pf, overflow);
   ++*L.counter;
 }

@@ -143,13 +143,15 @@ struct Launch {
 
 // bl_pyramid.cu
 void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
-                     long long s_fstride, double* dst, int dw, int dh, long long d_fstride, int n);
+                     long long s_fstride, double* dst, int dw, int dh, long long d_pitch, long long d_fstride, int n);
 // bl_hog.cu
 void set_direction_table(const double* ux, const double* uy);
 void launch_grad(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, int s_lo, int s_hi, const void* base,
                  int src_kind /*0 u8, 1 f64*/, double* fmag, uint8_t* fori);
 void launch_gradhist(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, const double* fmag,
                      const uint8_t* fori, double* bins, double* energy);
+void launch_hog(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, int s_lo, int s_hi, const void* base,
+                int src_kind /*0 u8, 1 f64*/, double* bins, double* energy);
 void launch_orientation(const Launch& L, const double* gx, const double* gy, long long n, uint8_t* out);
 void launch_sqrt_check(const Launch& L, const double* in, long long n, double* fast, double* ieee);
 void launch_energy(const Launch& L, const double* bins, long long cells, double* energy);

@@ -17,7 +17,7 @@ constexpr int kRsRows = 4;  // output rows per thread (column terms computed onc
 template <typename Tin>
 __global__ void __launch_bounds__(256) k_resample(const Tin* __restrict__ src, int sw, int sh,
                                                   long long s_pitch, long long s_fstride,
-                                                  double* __restrict__ dst, int dw, int dh,
+                                                  double* __restrict__ dst, int dw, int dh, long long d_pitch,
                                                   long long d_fstride, double rx, double ry) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y_first = (blockIdx.y * blockDim.y + threadIdx.y) * kRsRows;
@@ -50,21 +50,22 @@ __global__ void __launch_bounds__(256) k_resample(const Tin* __restrict__ src, i
     const double e = (double)__ldg(s + y1 * s_pitch + x1);
     const double top = dadd(dmul(a, gx), dmul(b, fx));
     const double bot = dadd(dmul(c, gx), dmul(e, fx));
-    d[(long long)y * dw + x] = dadd(dmul(top, dsub(1.0, fy)), dmul(bot, fy));
+    d[(long long)y * d_pitch + x] = dadd(dmul(top, dsub(1.0, fy)), dmul(bot, fy));
   }
 }
 
 void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
-                     long long s_fstride, double* dst, int dw, int dh, long long d_fstride, int n) {
+                     long long s_fstride, double* dst, int dw, int dh, long long d_pitch, long long d_fstride,
+                     int n) {
   const double rx = double(sw) / dw, ry = double(sh) / dh;  // image.cpp:136-137
   const dim3 block(32, 8);
   const dim3 grid((unsigned)div_up(dw, 32), (unsigned)div_up(dh, 8 * kRsRows), (unsigned)n);
   if (src_u8)
     k_resample<uint8_t><<<grid, block, 0, L.st>>>((const uint8_t*)src, sw, sh, s_pitch, s_fstride, dst, dw, dh,
-                                                   d_fstride, rx, ry);
+                                                   d_pitch, d_fstride, rx, ry);
   else
     k_resample<double><<<grid, block, 0, L.st>>>((const double*)src, sw, sh, s_pitch, s_fstride, dst, dw, dh,
-                                                  d_fstride, rx, ry);
+                                                  d_pitch, d_fstride, rx, ry);
   ++*L.counter;
 }
 
