@@ -21,7 +21,7 @@ LIB      := $(PKG)/libblinkline_b200.so
 CPPLIB   := $(PKG)/libblinkline_gpu.so
 
 EXACT_CU := bl_pyramid bl_hog bl_exact bl_ert
-FAST_CU  := bl_classify bl_capi
+FAST_CU  := bl_classify bl_screen_tc bl_capi
 OBJS     := $(addprefix $(BUILD)/,$(addsuffix .o,$(EXACT_CU) $(FAST_CU)))
 HDRS     := $(CSRC)/bl_internal.cuh include/blinkline_b200.h
 

@@ -97,6 +97,13 @@ int bl_ctx_enable_stage_timing(bl_ctx* ctx, int enable);
 int bl_ctx_stage_times(bl_ctx* ctx, float* ms /* BL_STAGE_COUNT */, int* launches /* BL_STAGE_COUNT */);
 /* Capture each (geometry, batch) pipeline into a CUDA graph and replay it (default on). */
 int bl_ctx_enable_graphs(bl_ctx* ctx, int enable);
+/* Classifier screen implementation (both feed the same exact fp64 re-score, so detections
+ * are bit-identical either way): BL_SCREEN_TCGEN05 -- implicit GEMM on the tensor cores
+ * (tcgen05.mma kind::tf32, default); BL_SCREEN_FP32 -- register-tiled CUDA-core FMA.  The
+ * environment variable BL_SCREEN=fp32|tc overrides the default at context creation. */
+#define BL_SCREEN_TCGEN05 0
+#define BL_SCREEN_FP32 1
+int bl_ctx_set_screen(bl_ctx* ctx, int mode);
 
 /* ------------------------------------------------------------------- models ---- */
 /* replaces: the DetectorModel value passed to detect_faces (detector.hpp:31-41,87).
@@ -187,6 +194,11 @@ int bl_orientation_bins(bl_ctx* ctx, const double* gx, const double* gy, int64_t
 /* Self-check of the device gradient-magnitude square root (sqrt_fast, bl_hog.cu) against
  * IEEE __dsqrt_rn on the same inputs (inputs in [1e-300, 1e300]). */
 int bl_debug_sqrt(bl_ctx* ctx, const double* in, int64_t n, double* fast, double* ieee);
+/* Raw tcgen05 screen sums (filter r, without bias) of every anchor of one feature image
+ * (cells_w x cells_h x 31 doubles) against the uploaded detector: scores[r][sh][sw], with
+ * the rigorous per-filter error bound the candidate cut uses in delta[r]. */
+int bl_debug_screen_tc(bl_ctx* ctx, const double* features, int cells_w, int cells_h, float* scores,
+                       double* delta);
 
 #ifdef __cplusplus
 }

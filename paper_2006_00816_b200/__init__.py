@@ -51,6 +51,7 @@ assert DET_DTYPE.itemsize == 32
 
 BL_OK, BL_ERR_INVALID, BL_ERR_MODEL, BL_ERR_CUDA, BL_ERR_CAPACITY, BL_ERR_STATE = range(6)
 BL_PIX_U8, BL_PIX_F64 = 0, 1
+SCREEN_TCGEN05, SCREEN_FP32 = 0, 1
 STAGES = ["h2d", "pyramid", "gradhist", "features", "screen", "rescore", "nms", "ert", "d2h"]
 
 
@@ -80,6 +81,7 @@ _SIGS = {
     "bl_ctx_enable_stage_timing": (C.c_int, [_vp, C.c_int]),
     "bl_ctx_stage_times": (C.c_int, [_vp, _P(C.c_float), _P(C.c_int)]),
     "bl_ctx_enable_graphs": (C.c_int, [_vp, C.c_int]),
+    "bl_ctx_set_screen": (C.c_int, [_vp, C.c_int]),
     "bl_detector_upload": (C.c_int, [_vp, _vp, _vp, _dbl, C.c_int, C.c_int, C.c_int, C.c_int, _dbl]),
     "bl_ert_upload": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _dbl, _vp, _vp, _vp, _vp]),
     "bl_detect": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _sz, _sz, _vp, _i64, _vp, _P(_i64)]),
@@ -101,6 +103,7 @@ _SIGS = {
     "bl_nms": (C.c_int, [_vp, _vp, _i64, _dbl, _vp, _P(_i64)]),
     "bl_orientation_bins": (C.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "bl_debug_sqrt": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "bl_debug_screen_tc": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)
@@ -399,6 +402,20 @@ class Context:
         _err(lib.bl_nms(self._h, dets.ctypes.data if len(dets) else None, len(dets), float(iou_threshold),
                         out.ctypes.data, C.byref(kept)))
         return out[:kept.value].copy()
+
+    def set_screen(self, mode):
+        """'tc' (tcgen05 implicit GEMM, default) or 'fp32' (CUDA-core FMA) classifier screen."""
+        _err(lib.bl_ctx_set_screen(self._h, {"tc": SCREEN_TCGEN05, "fp32": SCREEN_FP32}[mode]))
+
+    def debug_screen_tc(self, features):
+        """Raw tcgen05 screen sums of every anchor of one feature image (ch, cw, 31) against the
+        uploaded detector: (scores[5][sh][sw] float32, delta[5] rigorous error bounds)."""
+        f = _np(features, np.float64)
+        ch, cw = f.shape[0], f.shape[1]
+        sc = np.zeros((5, ch - 9, cw - 9), np.float32)
+        dl = np.zeros(5, np.float64)
+        _err(lib.bl_debug_screen_tc(self._h, f.ctypes.data, cw, ch, sc.ctypes.data, dl.ctypes.data))
+        return sc, dl
 
     def debug_sqrt(self, x):
         x = _np(x, np.float64).ravel()

@@ -103,6 +103,16 @@ bool is_device_ptr(const void* p) {
 
 int round_half_up_host(double v) { return int(std::floor(v + 0.5)); }  // detector.cpp:41
 
+// Round a float to the nearest tf32 value (ties away from zero, like cvt.rna.tf32.f32).
+float tf32_round_host(float x) {
+  uint32_t b;
+  std::memcpy(&b, &x, 4);
+  if ((b & 0x7f800000u) != 0x7f800000u) b = (b + 0x1000u) & ~0x1fffu;
+  float r;
+  std::memcpy(&r, &b, 4);
+  return r;
+}
+
 struct DetectorState {
   bool ready = false;
   double thr = 0;
@@ -110,7 +120,9 @@ struct DetectorState {
   double min_face_ratio = 0.2;
   double bias[kFilters] = {0};
   float cut[kFilters] = {0};
-  DevBuf w64, w32, bias64, cut32;
+  float cut_tc[kFilters] = {0};
+  double delta_tc[kFilters] = {0};
+  DevBuf w64, w32, bias64, cut32, w_tc, cuttc;
 };
 
 struct ErtState {
@@ -125,6 +137,7 @@ struct Plan {
   int n = 0, w = 0, h = 0, pix = 0;
   int window = 80, cell_px = 8, window_cells = 10, scale_num = 5, scale_den = 6;
   double min_face_ratio = 0.2;
+  int screen = BL_SCREEN_TCGEN05;
   int n_levels = 0;
   std::vector<int> lw, lh;
   std::vector<long long> arena_off;  // levels >= 1, in doubles
@@ -137,7 +150,7 @@ struct Plan {
   long long cand_cap = 0;
   long long f32_elems = 0;
   long long gkeys_pf = 0;
-  DevBuf arena, bins, energy, feat64, feat32, cand, n_cand, dets, det_count, kept, kept_count, gkeys,
+  DevBuf arena, bins, energy, feat64, feat32, feat_tc, cand, n_cand, dets, det_count, kept, kept_count, gkeys,
       overflow, offsets;
 };
 
@@ -184,6 +197,7 @@ struct bl_ctx {
   Slot slots[2];
   uint64_t next_ticket = 1;
   int face_cap_per_frame = 64;  // device-side capacity of landmarked faces per frame
+  int screen = BL_SCREEN_TCGEN05;
 };
 
 namespace {
@@ -212,7 +226,8 @@ void pyramid_dims(int w, int h, int window, std::vector<int>& lw, std::vector<in
 
 int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
   const DetectorState& D = c->det;
-  if (P.valid && P.n == n && P.w == w && P.h == h && P.pix == pix && P.window_cells == D.window_cells &&
+  if (P.valid && P.n == n && P.w == w && P.h == h && P.pix == pix && P.screen == c->screen &&
+      P.window_cells == D.window_cells &&
       P.cell_px == D.cell_px && P.scale_num == D.scale_num && P.scale_den == D.scale_den &&
       P.min_face_ratio == D.min_face_ratio)
     return BL_OK;
@@ -221,6 +236,7 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
   P.w = w;
   P.h = h;
   P.pix = pix;
+  P.screen = c->screen;
   P.window_cells = D.window_cells;
   P.cell_px = D.cell_px;
   P.scale_num = D.scale_num;
@@ -256,7 +272,7 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
   std::memset(&H, 0, sizeof H);
   H.n_frames = n;
   H.n_scored = (int)P.scored.size();
-  long long cells = 0, gh = 0, sc = 0, f32 = 0, anchors_pf = 0, fld = 0, gr = 0;
+  long long cells = 0, gh = 0, sc = 0, f32 = 0, anchors_pf = 0, fld = 0, gr = 0, ftc = 0;
   for (int s = 0; s < H.n_scored; ++s) {
     const int k = P.scored[s];
     LevelDesc& L = H.lv[s];
@@ -298,6 +314,8 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
     L.f32_off = f32;
     L.f32_fstride = (long long)kFeatPad * L.ch_pad * L.cw_pad;
     f32 += (long long)n * L.f32_fstride;
+    L.tc_off = ftc;
+    ftc += (long long)n * (long long)tc_feat_floats_per_frame(L.cw, L.ch, &L.tc_ncp, nullptr);
     L.fld_off = fld;
     fld += (long long)n * L.w * L.h;
     L.gr_tiles_x = (int)div_up(L.w, 32);
@@ -332,9 +350,15 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
   TRY(P.energy.ensure(sizeof(double) * std::max<long long>(1, cells)));
   TRY(P.feat64.ensure(sizeof(double) * kFeat * std::max<long long>(1, cells)));
   // zero once: the padding of the fp32 planes is never written by the feature kernel
-  const bool regrow = P.feat32.bytes < sizeof(float) * (size_t)std::max<long long>(1, f32);
-  TRY(P.feat32.ensure(sizeof(float) * std::max<long long>(1, f32), true));
-  if (!regrow) CK(cudaMemset(P.feat32.p, 0, sizeof(float) * std::max<long long>(1, f32)));
+  if (P.screen == BL_SCREEN_FP32) {
+    const bool regrow = P.feat32.bytes < sizeof(float) * (size_t)std::max<long long>(1, f32);
+    TRY(P.feat32.ensure(sizeof(float) * std::max<long long>(1, f32), true));
+    if (!regrow) CK(cudaMemset(P.feat32.p, 0, sizeof(float) * std::max<long long>(1, f32)));
+  } else {  // the zero tail of each tc plane is never written by the feature kernel
+    const bool regrow = P.feat_tc.bytes < sizeof(float) * (size_t)std::max<long long>(1, ftc);
+    TRY(P.feat_tc.ensure(sizeof(float) * std::max<long long>(1, ftc), true));
+    if (!regrow) CK(cudaMemset(P.feat_tc.p, 0, sizeof(float) * std::max<long long>(1, ftc)));
+  }
   TRY(P.cand.ensure(sizeof(Candidate) * P.cand_cap));
   TRY(P.n_cand.ensure(sizeof(unsigned long long)));
   TRY(P.dets.ensure(sizeof(DevDet) * n * P.cap_pf));
@@ -401,11 +425,16 @@ int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long lon
     launch_hog(L, P.host, Pd, s1, ns, P.arena.as<double>(), 1, P.bins.as<double>(), P.energy.as<double>());
   }
   stage_mark(c, BL_STAGE_FEATURES);
+  const bool tc = P.screen == BL_SCREEN_TCGEN05;
   launch_features(L, P.host, Pd, P.bins.as<double>(), P.energy.as<double>(), P.feat64.as<double>(),
-                  P.feat32.as<float>());
+                  tc ? nullptr : P.feat32.as<float>(), tc ? P.feat_tc.as<float>() : nullptr);
   stage_mark(c, BL_STAGE_SCREEN);
-  launch_screen(L, P.host, Pd, P.feat32.as<float>(), D.w32.as<float>(), D.cut32.as<float>(),
-                P.cand.as<Candidate>(), P.n_cand.as<unsigned long long>(), P.cand_cap);
+  if (tc)
+    launch_screen_tc(L, P.host, Pd, P.feat_tc.as<float>(), D.w_tc.as<float>(), D.cuttc.as<float>(),
+                     P.cand.as<Candidate>(), P.n_cand.as<unsigned long long>(), P.cand_cap, nullptr);
+  else
+    launch_screen(L, P.host, Pd, P.feat32.as<float>(), D.w32.as<float>(), D.cut32.as<float>(),
+                  P.cand.as<Candidate>(), P.n_cand.as<unsigned long long>(), P.cand_cap);
   stage_mark(c, BL_STAGE_RESCORE);
   launch_rescore(L, Pd, P.feat64.as<double>(), D.w64.as<double>(), D.bias64.as<double>(), D.thr, D.cell_px,
                  P.cand.as<Candidate>(), P.n_cand.as<unsigned long long>(), P.cand_cap, P.dets.as<DevDet>(),
@@ -818,6 +847,7 @@ int bl_ctx_create(int device, bl_ctx** out) {
     uy[d] = std::sin(a);
   }
   set_direction_table(ux, uy);
+  if (const char* e = std::getenv("BL_SCREEN")) c->screen = std::strcmp(e, "fp32") == 0 ? BL_SCREEN_FP32 : BL_SCREEN_TCGEN05;
   CK(cudaGetLastError());
   *out = c.release();
   return BL_OK;
@@ -883,6 +913,14 @@ int bl_ctx_stage_times(bl_ctx* c, float* ms, int* launches) {
   return BL_OK;
 }
 
+int bl_ctx_set_screen(bl_ctx* c, int mode) {
+  if (!c) return set_err(BL_ERR_INVALID, "null context");
+  if (mode != BL_SCREEN_TCGEN05 && mode != BL_SCREEN_FP32) return set_err(BL_ERR_INVALID, "unknown screen mode %d", mode);
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->screen = mode;
+  return BL_OK;
+}
+
 int bl_ctx_enable_graphs(bl_ctx* c, int enable) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
   c->graphs = enable != 0;
@@ -926,6 +964,33 @@ int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, d
     if ((double)cf > cutd) cf = std::nextafterf(cf, -INFINITY);
     D.cut[r] = cf;
   }
+  // tcgen05 screen: tf32 (round to nearest) weights [j][kc][64 n = dx * 5 + r][4], and the cut
+  // delta_tc >= |tf32 MMA sum - exact sum|: operands rounded to tf32 (each <= 2^-11 relative,
+  // product <= 2^-10 + 2^-22), fp32 feature rounding 2^-24, fp32 accumulation over 400
+  // MMAs of K = 8 (<= 1024 u even with truncating hardware adds), features <= 0.8486.
+  std::vector<float> wtc(tc_weight_floats(), 0.f);
+  for (int j = 0; j < kWin; ++j)
+    for (int dx = 0; dx < kWin; ++dx)
+      for (int f = 0; f < kFeat; ++f)
+        for (int r = 0; r < kFilters; ++r)
+          wtc[(((size_t)j * 8 + f / 4) * 64 + dx * kFilters + r) * 4 + f % 4] =
+              tf32_round_host((float)weights[(size_t)r * kFilterW + j * kRowW + dx * kFeat + f]);
+  for (int r = 0; r < kFilters; ++r) {
+    double l1 = 0;
+    for (int k = 0; k < kFilterW; ++k) l1 += std::fabs(weights[(size_t)r * kFilterW + k]);
+    const double rel = std::ldexp(1.0, -10) + std::ldexp(1.0, -22) + std::ldexp(1.0, -24) + 1024.0 * u;
+    const double delta = 1.1 * rel * 0.8486 * l1 + std::ldexp(1.0, -20) * (std::fabs(threshold) + std::fabs(biases[r])) + 1e-9;
+    D.delta_tc[r] = delta;
+    const double cutd = threshold - biases[r] - delta;
+    float cf = (float)cutd;
+    if (std::isnan(cutd)) cf = -INFINITY;
+    if ((double)cf > cutd) cf = std::nextafterf(cf, -INFINITY);
+    D.cut_tc[r] = cf;
+  }
+  TRY(D.w_tc.ensure(sizeof(float) * wtc.size()));
+  TRY(D.cuttc.ensure(sizeof(float) * kFilters));
+  CK(cudaMemcpy(D.w_tc.p, wtc.data(), sizeof(float) * wtc.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(D.cuttc.p, D.cut_tc, sizeof(float) * kFilters, cudaMemcpyHostToDevice));
   TRY(D.w64.ensure(sizeof(double) * kFilters * kFilterW));
   TRY(D.w32.ensure(sizeof(float) * w32.size()));
   TRY(D.bias64.ensure(sizeof(double) * kFilters));
@@ -1248,7 +1313,7 @@ int bl_compute_features(bl_ctx* c, const double* bins, const double* energy, int
   CK(cudaMemcpyAsync(c->s_desc.p, &H, sizeof H, cudaMemcpyHostToDevice, c->st));
   TRY(c->s_c.ensure(sizeof(double) * kFeat * cells));
   launch_features(launch_of(c), H, c->s_desc.as<PlanDesc>(), (const double*)b, (const double*)e,
-                  c->s_c.as<double>(), nullptr);
+                  c->s_c.as<double>(), nullptr, nullptr);
   return from_device(c, features, c->s_c.p, sizeof(double) * kFeat * cells);
 }
 
@@ -1273,7 +1338,7 @@ int bl_extract_features(bl_ctx* c, const double* image, int w, int h, double* fe
   const Launch L = launch_of(c);
   launch_hog(L, H, c->s_desc.as<PlanDesc>(), 0, 1, src, 1, c->s_b.as<double>(), c->s_c.as<double>());
   launch_features(L, H, c->s_desc.as<PlanDesc>(), c->s_b.as<double>(), c->s_c.as<double>(), c->s_d.as<double>(),
-                  nullptr);
+                  nullptr, nullptr);
   if (bins) CK(cudaMemcpyAsync(bins, c->s_b.p, sizeof(double) * kBins * cells, cudaMemcpyDefault, c->st));
   if (energy) CK(cudaMemcpyAsync(energy, c->s_c.p, sizeof(double) * cells, cudaMemcpyDefault, c->st));
   return from_device(c, features, c->s_d.p, sizeof(double) * kFeat * cells);
@@ -1344,6 +1409,38 @@ int bl_debug_sqrt(bl_ctx* c, const double* in, int64_t n, double* fast, double* 
   launch_sqrt_check(launch_of(c), (const double*)a, n, c->s_b.as<double>(), c->s_c.as<double>());
   CK(cudaMemcpyAsync(fast, c->s_b.p, sizeof(double) * n, cudaMemcpyDefault, c->st));
   return from_device(c, ieee, c->s_c.p, sizeof(double) * n);
+}
+
+
+int bl_debug_screen_tc(bl_ctx* c, const double* features, int cw, int ch, float* scores, double* delta) {
+  if (!c || !features || !scores) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->det.ready) return set_err(BL_ERR_STATE, "no detector model uploaded");
+  if (cw < kWin || ch < kWin) return set_err(BL_ERR_INVALID, "feature image smaller than the 10x10 detection window");
+  TRY(use_device(c));
+  PlanDesc H;
+  single_level_plan(H, cw * 8, ch * 8, cw, ch);
+  LevelDesc& Lv = H.lv[0];
+  const size_t nfl = tc_feat_floats_per_frame(cw, ch, &Lv.tc_ncp, nullptr);
+  Lv.tc_off = 0;
+  std::vector<float> host(nfl, 0.f);
+  for (long long cell = 0; cell < (long long)cw * ch; ++cell)
+    for (int f = 0; f < kFeat; ++f)
+      host[((size_t)(f / 4) * Lv.tc_ncp + cell) * 4 + f % 4] = tf32_round_host((float)features[cell * kFeat + f]);
+  const long long na = (long long)Lv.sw * Lv.sh;
+  TRY(c->s_a.ensure(sizeof(float) * nfl));
+  TRY(c->s_b.ensure(sizeof(float) * kFilters * na));
+  TRY(c->s_c.ensure(sizeof(Candidate) * kFilters * na + sizeof(unsigned long long)));
+  TRY(c->s_desc.ensure(sizeof(PlanDesc)));
+  CK(cudaMemcpyAsync(c->s_a.p, host.data(), sizeof(float) * nfl, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->s_desc.p, &H, sizeof H, cudaMemcpyHostToDevice, c->st));
+  unsigned long long* nc = reinterpret_cast<unsigned long long*>(c->s_c.as<Candidate>() + kFilters * na);
+  CK(cudaMemsetAsync(nc, 0, sizeof(unsigned long long), c->st));
+  launch_screen_tc(launch_of(c), H, c->s_desc.as<PlanDesc>(), c->s_a.as<float>(), c->det.w_tc.as<float>(),
+                   c->det.cuttc.as<float>(), c->s_c.as<Candidate>(), nc, kFilters * na, c->s_b.as<float>());
+  if (delta)
+    for (int r = 0; r < kFilters; ++r) delta[r] = c->det.delta_tc[r];
+  return from_device(c, scores, c->s_b.p, sizeof(float) * kFilters * na);
 }
 
 }  // extern "C"

@@ -59,6 +59,8 @@ struct LevelDesc {
                                // (4 * sc_lanes_x) x (32 / sc_lanes_x) anchors
   long long sc_begin;          // first screening warp-tile id of this level
   long long cell_begin;        // first cell id (for per-cell kernels) of this level
+  long long tc_off;            // tcgen05 screen features: float offset of frame 0 ([8 planes][tc_ncp][4])
+  long long tc_ncp;            // cells per plane (linear index cy * cw + cx, zero-padded tail)
   long long anchor_base;       // per-frame anchor offset (for candidate records)
 };
 
@@ -156,11 +158,17 @@ void launch_orientation(const Launch& L, const double* gx, const double* gy, lon
 void launch_sqrt_check(const Launch& L, const double* in, long long n, double* fast, double* ieee);
 void launch_energy(const Launch& L, const double* bins, long long cells, double* energy);
 void launch_features(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, const double* bins,
-                     const double* energy, double* feat64, float* feat32);
+                     const double* energy, double* feat64, float* feat32, float* feat_tc);
 // bl_classify.cu
 void launch_screen(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, const float* feat32,
                    const float* w32, const float* cut, Candidate* cand, unsigned long long* n_cand,
                    long long cand_cap);
+// bl_screen_tc.cu
+size_t tc_feat_floats_per_frame(int cw, int ch, long long* ncp_out, int* tiles_out);
+size_t tc_weight_floats();
+void launch_screen_tc(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, const float* feat_tc,
+                      const float* w_tc, const float* cut, Candidate* cand, unsigned long long* n_cand,
+                      long long cand_cap, float* dbg_scores);
 // bl_exact.cu
 void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, const double* w64,
                     const double* bias, double thr, int cell_px, const Candidate* cand,
