@@ -103,6 +103,8 @@ bool is_device_ptr(const void* p) {
 
 int round_half_up_host(double v) { return int(std::floor(v + 0.5)); }  // detector.cpp:41
 
+constexpr int kLevelMargin = 8;  // readable doubles either side of every arena level row
+
 // Round a float to the nearest tf32 value (ties away from zero, like cvt.rna.tf32.f32).
 float tf32_round_host(float x) {
   uint32_t b;
@@ -249,11 +251,14 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
   P.arena_off.assign(P.n_levels, 0);
   P.lpitch.assign(P.n_levels, 0);
   long long off = 0;
+  // level rows: 8-element margins either side and a pitch of a multiple of 4 doubles, so
+  // k_hog reads 16-B aligned 8-pixel groups straddling the image edge without clamping
   for (int k = 1; k < P.n_levels; ++k) {
-    P.lpitch[k] = (int)div_up(P.lw[k], 4) * 4;  // 32-B aligned rows: 16-B vector loads in k_hog
-    P.arena_off[k] = off;
+    P.lpitch[k] = (int)div_up(P.lw[k] + 2 * kLevelMargin, 4) * 4;
+    P.arena_off[k] = off + kLevelMargin;
     off += (long long)n * P.lpitch[k] * P.lh[k];
   }
+  off += 2 * kLevelMargin;
   P.arena_elems = off;
 
   // eligible_scales (detector.cpp:144-155) + the "room for a window" skip (:165-167)
@@ -293,6 +298,7 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
       L.pix_off = P.arena_off[k];
       L.pix_fstride = (long long)P.lpitch[k] * L.h;
       L.pix_pitch = P.lpitch[k];
+      L.pix_margin = kLevelMargin;
     }
     L.cell_off = cells;
     L.cell_begin = cells;

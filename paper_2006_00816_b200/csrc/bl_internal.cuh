@@ -44,6 +44,7 @@ struct LevelDesc {
   long long pix_off;     // level pixels: element offset of frame 0 in the level arena
   long long pix_fstride; // elements between frames
   int pix_pitch;         // elements between rows
+  int pix_margin;        // readable elements left of x = 0 and right of x = w - 1 on every row
   long long cell_off;    // cells: offset of frame 0 in the cell arenas (bins/energy/feat64)
   long long f32_off;     // fp32 planar features: float offset of frame 0
   int cw_pad, ch_pad;    // fp32 planar plane dims
