@@ -156,10 +156,18 @@ struct Plan {
       overflow, offsets;
 };
 
+// ERT cascade working set (current shapes, per-level transforms, leaf-index scratch).
+struct ErtWork {
+  DevBuf cur, tf, leafs;
+};
+
 // One in-flight batch: its staged input, its device results and pinned host mirrors.  Two
-// slots let batch i+1's H2D and batch i's result copies overlap compute (bl_submit/collect).
+// slots let batch i+1's H2D, detection, and batch i's landmark cascade and result copies
+// overlap (bl_submit/collect).
 struct Slot {
   DevBuf input, flat, face_frame, meta, ert_out;
+  ErtWork ert;                  // the slot's cascade runs on the ERT stream, beside the next detect
+  cudaEvent_t ev_det = nullptr; // detections flattened: the ERT stream may start
   int* h_meta = nullptr;
   size_t h_meta_cap = 0;
   void* h_stage = nullptr;
@@ -184,7 +192,8 @@ struct bl_ctx {
   ErtState ert;
   Plan plan;
   // ERT working set
-  DevBuf ert_cur, ert_out, ert_leaf, ert_leafs, ert_tf, ert_boxes, ert_frames, ert_nfaces, ert_err, ert_input;
+  ErtWork ert_work;  // bl_landmarks' cascade (on the compute stream)
+  DevBuf ert_out, ert_leaf, ert_boxes, ert_frames, ert_nfaces, ert_err, ert_input;
   // scratch for stage functions
   DevBuf s_a, s_b, s_c, s_d, s_e, s_desc;
   // pinned host staging for counts
@@ -196,6 +205,7 @@ struct bl_ctx {
   int stage_launch[BL_STAGE_COUNT] = {};
   bool graphs = true;
   cudaStream_t hst = nullptr;  // H2D stream (input frames): never queued behind a D2H wait
+  cudaStream_t est = nullptr;  // ERT stream: batch i's cascade overlaps batch i+1's detection
   Slot slots[2];
   uint64_t next_ticket = 1;
   int face_cap_per_frame = 64;  // device-side capacity of landmarked faces per frame
@@ -499,29 +509,29 @@ int check_frames(const void* frames, int pix, int n, int w, int h, size_t pitch,
 
 // Runs the ERT cascade for `nf` faces whose boxes (int stride) and frame indices are on the
 // device; n_faces_dev holds the count.  Output landmarks -> c->ert_out.
-int run_ert(bl_ctx* c, const void* frames, int pix, int w, int h, long long pitch, long long fstride,
-            const int* face_frame, const int* boxes, int box_stride, const int* n_faces_dev, int nf,
-            uint8_t* leaf_dev, double* out_xy, int* err_dev) {
+int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix, int w, int h, long long pitch,
+            long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces_dev,
+            int nf, uint8_t* leaf_dev, double* out_xy, int* err_dev) {
   ErtState& E = c->ert;
-  const Launch L = launch_of(c);
+  const Launch L{st, &c->launches};
   const int L2 = 2 * E.dev.L;
-  TRY(c->ert_cur.ensure(sizeof(double) * L2 * std::max(1, nf)));
-  TRY(c->ert_tf.ensure(sizeof(double2) * std::max(1, nf)));
+  TRY(wk.cur.ensure(sizeof(double) * L2 * std::max(1, nf)));
+  TRY(wk.tf.ensure(sizeof(double2) * std::max(1, nf)));
   // leaf indices: the caller's [face][T*K] buffer, else a per-level scratch [face][K]
   long long leaf_stride = (long long)E.dev.T * E.dev.K;
   uint8_t* leaf = leaf_dev;
   if (!leaf) {
     leaf_stride = div_up(E.dev.K, 16) * 16;  // 16-B aligned rows: 128-bit index loads
-    TRY(c->ert_leafs.ensure((size_t)std::max(1, nf) * leaf_stride + 16));
-    leaf = c->ert_leafs.as<uint8_t>();
+    TRY(wk.leafs.ensure((size_t)std::max(1, nf) * leaf_stride + 16));
+    leaf = wk.leafs.as<uint8_t>();
   }
-  CK(cudaMemsetAsync(err_dev, 0, sizeof(int), c->st));
-  launch_ert_init(L, E.dev, n_faces_dev, nf, c->ert_cur.as<double>());
+  CK(cudaMemsetAsync(err_dev, 0, sizeof(int), st));
+  launch_ert_init(L, E.dev, n_faces_dev, nf, wk.cur.as<double>());
   for (int t = 0; t < E.dev.T; ++t)
     launch_ert_level(L, E.dev, t, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
-                     n_faces_dev, nf, c->ert_cur.as<double>(), c->ert_tf.as<double2>(),
+                     n_faces_dev, nf, wk.cur.as<double>(), wk.tf.as<double2>(),
                      leaf_dev ? leaf + (long long)t * E.dev.K : leaf, leaf_stride, err_dev);
-  launch_ert_finish(L, E.dev, boxes, box_stride, n_faces_dev, nf, c->ert_cur.as<double>(), out_xy);
+  launch_ert_finish(L, E.dev, boxes, box_stride, n_faces_dev, nf, wk.cur.as<double>(), out_xy);
   return BL_OK;
 }
 
@@ -575,6 +585,7 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
   if (!same) {  // arenas may be reallocated: nothing may still be reading them
     CK(cudaStreamSynchronize(c->st));
     CK(cudaStreamSynchronize(c->hst));
+    CK(cudaStreamSynchronize(c->est));
     for (Slot& o : c->slots) CK(cudaStreamSynchronize(o.d2h));
   }
   timing_begin(c);
@@ -613,12 +624,20 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
   if (landmarks) {
     TRY(S.ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * cap_faces));
     stage_mark(c, BL_STAGE_ERT);
-    TRY(run_ert(c, dev, pix, w, h, dp, df, S.face_frame.as<int>(), S.flat.as<int>(), 8, meta + n, (int)cap_faces,
-                nullptr, S.ert_out.as<double>(), meta + n + 2));
+    // the cascade only reads this slot's buffers and the frames, so (unless per-stage timing
+    // wants one ordered stream) it runs on the ERT stream while the next batch detects
+    cudaStream_t es = c->timing ? c->st : c->est;
+    if (es != c->st) {
+      CK(cudaEventRecord(S.ev_det, c->st));
+      CK(cudaStreamWaitEvent(es, S.ev_det, 0));
+    }
+    TRY(run_ert(c, es, S.ert, dev, pix, w, h, dp, df, S.face_frame.as<int>(), S.flat.as<int>(), 8, meta + n,
+                (int)cap_faces, nullptr, S.ert_out.as<double>(), meta + n + 2));
+    CK(cudaEventRecord(S.ev_done, es));
   } else {
     CK(cudaMemsetAsync(meta + n + 2, 0, sizeof(int), c->st));
+    CK(cudaEventRecord(S.ev_done, c->st));
   }
-  CK(cudaEventRecord(S.ev_done, c->st));
   // counts + flags back on the slot's D2H stream as soon as compute finishes
   TRY(ensure_pinned(reinterpret_cast<void*&>(S.h_meta), S.h_meta_cap, sizeof(int) * (n + 4)));
   CK(cudaStreamWaitEvent(S.d2h, S.ev_done, 0));
@@ -836,10 +855,12 @@ int bl_ctx_create(int device, bl_ctx** out) {
   c->device = device;
   CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->hst, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->est, cudaStreamNonBlocking));
   c->st = c->own;
   for (Slot& S : c->slots) {
     CK(cudaStreamCreateWithFlags(&S.d2h, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&S.ev_h2d, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&S.ev_det, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&S.ev_done, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&S.ev_meta, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&S.ev_out, cudaEventDisableTiming));
@@ -864,24 +885,26 @@ void bl_ctx_destroy(bl_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   if (c->hst) cudaStreamSynchronize(c->hst);
+  if (c->est) cudaStreamSynchronize(c->est);
   if (c->h_counts) cudaFreeHost(c->h_counts);
   for (Slot& S : c->slots) {
     if (S.h_meta) cudaFreeHost(S.h_meta);
     if (S.h_stage) cudaFreeHost(S.h_stage);
-    for (cudaEvent_t e : {S.ev_h2d, S.ev_done, S.ev_meta, S.ev_out})
+    for (cudaEvent_t e : {S.ev_h2d, S.ev_det, S.ev_done, S.ev_meta, S.ev_out})
       if (e) cudaEventDestroy(e);
     if (S.d2h) {
       cudaStreamSynchronize(S.d2h);
       cudaStreamDestroy(S.d2h);
     }
   }
-  cudaStream_t hst = c->hst;
+  cudaStream_t hst = c->hst, est = c->est;
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t own = c->own;
   delete c;  // DevBufs free on their device
   if (own) cudaStreamDestroy(own);
   if (hst) cudaStreamDestroy(hst);
+  if (est) cudaStreamDestroy(est);
 }
 
 int bl_ctx_set_stream(bl_ctx* c, void* stream) {
@@ -895,6 +918,8 @@ int bl_ctx_synchronize(bl_ctx* c) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
   TRY(use_device(c));
   CK(cudaStreamSynchronize(c->st));
+  CK(cudaStreamSynchronize(c->est));
+  CK(cudaStreamSynchronize(c->hst));
   return BL_OK;
 }
 
@@ -1172,7 +1197,7 @@ int bl_landmarks(bl_ctx* c, const void* frames, int pixel_type, int n_frames, in
   stage_mark(c, BL_STAGE_ERT);
   TRY(c->ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * std::max(1, nf)));
   TRY(c->ert_err.ensure(sizeof(int)));
-  TRY(run_ert(c, dev, pixel_type, w, h, dp, df, c->ert_frames.as<int>(), c->ert_boxes.as<int>(), 4,
+  TRY(run_ert(c, c->st, c->ert_work, dev, pixel_type, w, h, dp, df, c->ert_frames.as<int>(), c->ert_boxes.as<int>(), 4,
               c->ert_nfaces.as<int>(), nf, leaf_dev, c->ert_out.as<double>(), c->ert_err.as<int>()));
   stage_mark(c, BL_STAGE_D2H);
   CK(cudaMemcpyAsync(out_xy, c->ert_out.p, sizeof(double) * 2 * c->ert.dev.L * n_boxes, cudaMemcpyDefault, c->st));
