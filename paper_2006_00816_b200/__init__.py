@@ -36,7 +36,9 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-library_path = os.path.join(_HERE, "libblinkline_b200.so")
+# BL_LIBRARY selects an alternative build of the same library (kernel-variant experiments,
+# tools/build_variant.sh); there is no CPU fallback either way.
+library_path = os.environ.get("BL_LIBRARY") or os.path.join(_HERE, "libblinkline_b200.so")
 
 if not os.path.exists(library_path):
     raise ImportError(

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Build an experimental variant of libblinkline_b200.so with extra -D flags into
+# variants/NAME/ (git-ignored; travels to the GPU box).  Select it with BL_LIBRARY.
+#   bash tools/build_variant.sh NAME "-DBL_HOG_BATCH=1 -DBL_HOG_MINBLOCKS=5"
+set -e
+NAME=$1; DEFS=$2
+ROOT=$(cd "$(dirname "$0")/.." && pwd)
+OUT=$ROOT/variants/$NAME; mkdir -p $OUT
+ARCH="-gencode arch=compute_100a,code=sm_100a"
+FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $DEFS"
+C=$ROOT/paper_2006_00816_b200/csrc
+for f in bl_pyramid bl_hog bl_exact bl_ert; do nvcc $FL --fmad=false -c $C/$f.cu -o $OUT/$f.o & done
+for f in bl_classify bl_screen_tc bl_capi; do nvcc $FL -c $C/$f.cu -o $OUT/$f.o & done
+wait
+nvcc $ARCH -shared -o $OUT/libblinkline_b200.so $OUT/*.o -Xcompiler -fPIC -lcudart_static -lrt -lpthread -ldl
+rm -f $OUT/*.o
+echo "built $OUT/libblinkline_b200.so"
