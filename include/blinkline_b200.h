@@ -143,9 +143,10 @@ int bl_detect_landmarks(bl_ctx* ctx, const void* frames, int pixel_type, int n, 
  * pipelined run(), pipeline.cpp:230-324): bl_submit enqueues a batch (H2D of host frames on
  * a copy stream, the whole detect [+ landmark] pipeline on the compute stream, result
  * metadata back) and returns at once; bl_collect waits for it and copies its results out
- * exactly like bl_detect / bl_detect_landmarks.  Up to two batches may be in flight, so the
- * next batch's H2D and the previous batch's result copies overlap compute.  Tickets are
- * collected in submission order. */
+ * exactly like bl_detect / bl_detect_landmarks.  Up to BL_MAX_IN_FLIGHT batches may be in
+ * flight, so later batches' H2D, the landmark cascade of an earlier one (its own stream) and
+ * result copies overlap detection.  Tickets are collected in submission order. */
+#define BL_MAX_IN_FLIGHT 3
 int bl_submit(bl_ctx* ctx, const void* frames, int pixel_type, int n, int w, int h, size_t pitch,
               size_t frame_stride, int with_landmarks, uint64_t* ticket);
 int bl_collect(bl_ctx* ctx, uint64_t ticket, bl_detection* out, int64_t cap, int32_t* counts,

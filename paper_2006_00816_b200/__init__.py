@@ -54,6 +54,7 @@ assert DET_DTYPE.itemsize == 32
 BL_OK, BL_ERR_INVALID, BL_ERR_MODEL, BL_ERR_CUDA, BL_ERR_CAPACITY, BL_ERR_STATE = range(6)
 BL_PIX_U8, BL_PIX_F64 = 0, 1
 SCREEN_TCGEN05, SCREEN_FP32 = 0, 1
+MAX_IN_FLIGHT = 3  # BL_MAX_IN_FLIGHT
 STAGES = ["h2d", "pyramid", "gradhist", "features", "screen", "rescore", "nms", "ert", "d2h"]
 
 
@@ -273,7 +274,8 @@ class Context:
         or with flat=True (dets, counts, landmarks) back to back."""
         return self._sync_call(frames, True, cap, flat)
 
-    # pipelined mode: up to two batches in flight (H2D / result copies overlap compute)
+    # pipelined mode: up to MAX_IN_FLIGHT batches in flight (H2D, landmark cascade and result
+    # copies overlap detection)
     def submit(self, frames, landmarks=True):
         a, pix, n, h, w = _frames(frames)
         t = C.c_uint64(0)

@@ -161,9 +161,9 @@ struct ErtWork {
   DevBuf cur, tf, leafs;
 };
 
-// One in-flight batch: its staged input, its device results and pinned host mirrors.  Two
-// slots let batch i+1's H2D, detection, and batch i's landmark cascade and result copies
-// overlap (bl_submit/collect).
+// One in-flight batch: its staged input, its device results and pinned host mirrors.  Three
+// slots let batch i+2's H2D, batch i+1's detection, and batch i's landmark cascade and
+// result copies overlap (bl_submit/collect).
 struct Slot {
   DevBuf input, flat, face_frame, meta, ert_out;
   ErtWork ert;                  // the slot's cascade runs on the ERT stream, beside the next detect
@@ -206,7 +206,7 @@ struct bl_ctx {
   bool graphs = true;
   cudaStream_t hst = nullptr;  // H2D stream (input frames): never queued behind a D2H wait
   cudaStream_t est = nullptr;  // ERT stream: batch i's cascade overlaps batch i+1's detection
-  Slot slots[2];
+  Slot slots[BL_MAX_IN_FLIGHT];
   uint64_t next_ticket = 1;
   int face_cap_per_frame = 64;  // device-side capacity of landmarked faces per frame
   int screen = BL_SCREEN_TCGEN05;
@@ -717,7 +717,7 @@ int detect_common(bl_ctx* c, const void* frames, int pix, int n, int w, int h, s
     if (total) *total = 0;
     return BL_OK;
   }
-  for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < BL_MAX_IN_FLIGHT; ++s)
     if (c->slots[s].busy) return set_err(BL_ERR_STATE, "submitted batches must be collected first");
   for (int attempt = 0; attempt < 2; ++attempt) {
     TRY(enqueue(c, 0, frames, pix, n, w, h, pitch, fstride, landmarks != nullptr));
@@ -1138,8 +1138,9 @@ int bl_submit(bl_ctx* c, const void* frames, int pixel_type, int n, int w, int h
   if (n < 1) return set_err(BL_ERR_INVALID, "empty batch");
   TRY(use_device(c));
   const uint64_t t = c->next_ticket;
-  const int s = (int)(t & 1);
-  if (c->slots[s].busy) return set_err(BL_ERR_STATE, "two batches in flight: collect one before submitting");
+  const int s = (int)(t % BL_MAX_IN_FLIGHT);
+  if (c->slots[s].busy)
+    return set_err(BL_ERR_STATE, "%d batches in flight: collect one before submitting", BL_MAX_IN_FLIGHT);
   TRY(enqueue(c, s, frames, pixel_type, n, w, h, pitch, frame_stride, with_landmarks != 0));
   c->slots[s].ticket = t;
   c->next_ticket = t + 1;
@@ -1151,7 +1152,7 @@ int bl_collect(bl_ctx* c, uint64_t ticket, bl_detection* out, int64_t cap, int32
                double* landmarks) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
   std::lock_guard<std::mutex> lk(c->mu);
-  const int s = (int)(ticket & 1);
+  const int s = (int)(ticket % BL_MAX_IN_FLIGHT);
   if (!c->slots[s].busy || c->slots[s].ticket != ticket) return set_err(BL_ERR_STATE, "unknown or collected ticket");
   TRY(use_device(c));
   return collect(c, s, out, cap, counts, total, landmarks);

@@ -405,15 +405,19 @@ def test_submit_collect_matches_sync(ctx, pattern_model):
     b = ring_frames_np(5, 320, 240, seed=22)
     sa = ctx.detect_landmarks(a, flat=True)
     sb = ctx.detect_landmarks(b, flat=True)
+    import paper_2006_00816_b200 as bl
+    assert bl.MAX_IN_FLIGHT == 3
     ta = ctx.submit(a)
-    tb = ctx.submit(b)  # two in flight
+    tb = ctx.submit(b)
+    tx = ctx.submit(a)  # three in flight
     with pytest.raises(RuntimeError):
-        ctx.submit(a)  # a third would reuse a busy slot
+        ctx.submit(a)  # a fourth would reuse a busy slot
     ra = ctx.collect(ta)
     tc = ctx.submit(b)
     rb = ctx.collect(tb)
+    rx = ctx.collect(tx)
     rc = ctx.collect(tc)
-    for got, want in [(ra, sa), (rb, sb), (rc, sb)]:
+    for got, want in [(ra, sa), (rb, sb), (rx, sa), (rc, sb)]:
         assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
         assert np.array_equal(got[2], want[2])
     with pytest.raises(RuntimeError):
