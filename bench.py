@@ -247,12 +247,19 @@ def run_ours(args):
 
     # ---- roofline of the dominant stage
     alg = algorithmic_bytes_per_frame()
-    peaks = {}
+    peaks, peak_note = {}, "of fallback (B200_PROFILING.md: 6650 GB/s, 1590 bf16 TFLOP/s; MEASURED_PEAKS.json absent)"
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak_note = "of measured (MEASURED_PEAKS.json)"
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    tf32_peak = float(peaks.get("bf16_tflops", 1590.0)) / 2.0  # dense tf32 = half the bf16 rate
+    traffic = {}
+    try:  # ncu dram__bytes_read + write per frame of each stage's kernels (profiles/traffic.json)
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bytes_per_frame"]
+    except Exception:
+        pass
     kern_ms = {k: stages[k] for k in ("pyramid", "gradhist", "features", "screen", "rescore", "nms", "ert")}
     dom = max(kern_ms, key=kern_ms.get)
     ert_bytes = faces_per_step * ERT_T * ERT_K * (68 * 2 * 8 + ERT_F * 48 + ERT_F * 2)
@@ -260,24 +267,22 @@ def run_ours(args):
                    "screen": alg["screen"] * B, "ert": ert_bytes}
     per_stage = {}
     for k, ms in kern_ms.items():
+        e = {"ms": round(ms, 3)}
         if k in bytes_stage and ms > 0:
             gbs = bytes_stage[k] / (ms / 1000.0) / 1e9
-            per_stage[k] = {"ms": round(ms, 3), "GB/s": round(gbs, 1), "frac_hbm": round(gbs / hbm_peak, 3)}
-        else:
-            per_stage[k] = {"ms": round(ms, 3)}
-    if dom == "screen":
-        flops = 2 * 5 * 3100 * alg["anchors"] * B
-        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-        fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # nominal FP32 FMA peak at max clock
-        ach = flops / (kern_ms[dom] / 1000.0) / 1e12
-        roofline = {"bound": "fp32-fma", "achieved": round(ach, 2), "peak": round(fp32_peak, 1), "unit": "TFLOP/s",
-                    "frac": round(ach / fp32_peak, 3), "traffic": None,
-                    "peak_source": "nominal 148 SM x 128 FMA/clk x 2 at sm_max_mhz (no measured FP32 peak)"}
-    else:
-        ach = bytes_stage.get(dom, 0) / (kern_ms[dom] / 1000.0) / 1e9
-        roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
-                    "frac": round(ach / hbm_peak, 3), "traffic": None,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
+            e.update({"GB/s": round(gbs, 1), "frac_hbm": round(gbs / hbm_peak, 3)})
+        if k in traffic:
+            e["dram_GB_ncu"] = round(traffic[k] * B / 1e9, 3)
+        per_stage[k] = e
+    if kern_ms["screen"] > 0:  # the tcgen05 screen: useful FLOPs (dense 10x10x31 x 5 filters)
+        tfs = 2 * 5 * 3100 * alg["anchors"] * B / (kern_ms["screen"] / 1000.0) / 1e12
+        per_stage["screen"].update({"TFLOP/s": round(tfs, 1), "frac_tf32": round(tfs / tf32_peak, 3)})
+    ach = bytes_stage.get(dom, 0) / (kern_ms[dom] / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 3),
+                "traffic": round(traffic[dom] * B / 1e9, 3) if dom in traffic else None,
+                "traffic_unit": "GB per step (ncu dram__bytes_read+write.sum, profiles/traffic.json)",
+                "peak_source": peak_note}
     roofline["kernel"] = dom
 
     # ---- CPU baseline (rank 0, N=1): the reference library on this box's cores
