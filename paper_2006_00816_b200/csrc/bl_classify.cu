@@ -122,45 +122,16 @@ __global__ void __launch_bounds__(kScreenWarps * 32, 2) k_screen(const PlanDesc*
       for (int r = 0; r < kFilters; ++r) acc[q][r] += aj[q][r];
   }
 
-  // epilogue: threshold with the rigorous cut, warp-aggregated compaction
-  unsigned flags = 0;
-  int cnt = 0;
+  // epilogue: threshold with the rigorous cut, warp-aggregated append per filter list
   const bool row_ok = y < D.sh;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const bool ok = row_ok && (x + q) < D.sw;
+    unsigned flags = 0;
 #pragma unroll
-    for (int r = 0; r < kFilters; ++r) {
-      if (ok && acc[q][r] > __ldg(cut + r)) {
-        flags |= 1u << (q * kFilters + r);
-        ++cnt;
-      }
-    }
-  }
-  int incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const int warp_total = __shfl_sync(0xffffffffu, incl, 31);
-  if (warp_total == 0) return;
-  unsigned long long base = 0;
-  if (lane == 31) base = atomicAdd(n_cand, (unsigned long long)warp_total);
-  base = __shfl_sync(0xffffffffu, base, 31);
-  long long pos = (long long)base + incl - cnt;
-  while (flags) {
-    const int bit = __ffs(flags) - 1;
-    flags &= flags - 1;
-    if (pos < cap) {
-      Candidate c;
-      c.frame = f;
-      c.slot_r = s * 8 + bit % kFilters;
-      c.cx = x + bit / kFilters;
-      c.cy = y;
-      cand[pos] = c;
-    }
-    ++pos;
+    for (int r = 0; r < kFilters; ++r)
+      if (ok && acc[q][r] > __ldg(cut + r)) flags |= 1u << r;
+    emit_candidates(flags, f, s, x + q, y, cand, n_cand, cap);
   }
 }
 

@@ -9,6 +9,8 @@
 // operations, so the kept list is bit-identical to the reference's.
 #include <float.h>
 
+#include <algorithm>
+
 #include "bl_internal.cuh"
 
 namespace blb {
@@ -36,37 +38,48 @@ BL_DEV double exact_window_score3(const double* __restrict__ feat, int cw, int c
 
 BL_DEV int round_half_up(double v) { return (int)floor(dadd(v, 0.5)); }  // detector.cpp:41
 
-// The re-score proper.  A warp scores three candidates; lanes 10g + j (g < 3) own window
-// row j of candidate g and run its 310-term dot product strictly in the reference's order.
-// The operands are staged one window cell (31 features) at a time into padded shared memory
-// with coalesced loads -- lane f of the warp fetches feature/weight f of each of the 30
-// (candidate, row) strips -- so global traffic is 248-B contiguous segments instead of one
-// 8-B scalar per lane per term.  Row pitch 33 doubles keeps the 30 strips on distinct banks.
+// The re-score proper.  blockIdx.y = filter r: the CTA keeps W_r (fp64, rows padded to 311
+// doubles so the ten window rows sit on distinct banks) resident in shared memory and walks
+// that filter's candidate list.  A warp scores three candidates; lanes 10g + j (g < 3) own
+// window row j of candidate g and run its 310-term dot product strictly in the reference's
+// order.  The feature strips are staged one window cell (31 features) at a time into padded
+// shared memory with coalesced loads -- lane f of the warp fetches feature f of each of the
+// 30 (candidate, row) strips -- instead of one 8-B scalar per lane per term.
 constexpr int kRsPitch = 33;
-constexpr int kRsWarps = 4;
-constexpr int kRsWarpDoubles = 2 * 30 * kRsPitch;
-constexpr size_t kRsSmem = sizeof(double) * kRsWarps * kRsWarpDoubles;  // 63,360 B
+constexpr int kRsWPitch = kRowW + 1;  // 311
+constexpr int kRsWarps = 8;
+constexpr int kRsWarpDoubles = 30 * kRsPitch;
+constexpr size_t kRsSmem = sizeof(double) * ((size_t)kRsWarps * kRsWarpDoubles + (size_t)kWin * kRsWPitch);
 
 __global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __restrict__ P,
                                                  const double* __restrict__ feat64,
                                                  const double* __restrict__ w64,
                                                  const double* __restrict__ bias, double thr,
-                                                 int cell_px, const Candidate* __restrict__ cand,
+                                                 int cell_px, const Candidate* __restrict__ cand_all,
                                                  const unsigned long long* __restrict__ n_cand,
                                                  long long cand_cap, DevDet* __restrict__ dets,
                                                  int* __restrict__ det_count, long long cap_pf,
                                                  int* __restrict__ overflow) {
   extern __shared__ double rs_smem[];
+  const int r = blockIdx.y;
+  const long long n = min((long long)n_cand[r], cand_cap);
+  if (n == 0) return;
+  const Candidate* __restrict__ cand = cand_all + r * cand_cap;
+  double* Wsm = rs_smem + (size_t)kRsWarps * kRsWarpDoubles;  // [10][311]
+  for (int e = threadIdx.x; e < kFilterW; e += blockDim.x) {
+    const int j = e / kRowW;
+    Wsm[j * kRsWPitch + (e - j * kRowW)] = __ldg(w64 + (size_t)r * kFilterW + e);
+  }
+  __syncthreads();
+  const double br = bias[r];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* Fs = rs_smem + warp * kRsWarpDoubles;
-  double* Ws = Fs + 30 * kRsPitch;
   const int g = lane / 10;
-  const long long n = min((long long)*n_cand, cand_cap);
+  const int jl = lane - 10 * g;  // this lane's window row (lanes < 30)
   const long long nw = (long long)gridDim.x * kRsWarps;
   for (long long i0 = ((long long)blockIdx.x * kRsWarps + warp) * 3; i0 < n; i0 += nw * 3) {
     // strip bases of the three candidates (row 0 of the window, cell 0): every lane holds all
     const double* fst[3];
-    const double* wst[3];
     int cwv[3];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -74,25 +87,22 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __res
       const LevelDesc& D = P->lv[c.slot_r >> 3];
       cwv[q] = D.cw;
       fst[q] = feat64 + (D.cell_off + (long long)c.frame * D.cw * D.ch + (long long)c.cy * D.cw + c.cx) * kFeat;
-      wst[q] = w64 + (c.slot_r & 7) * kFilterW;
     }
     double acc = 0.0;
+    const double* wrow = Wsm + (lane < 30 ? jl : 0) * kRsWPitch;
 #pragma unroll 1
     for (int ci = 0; ci < kWin; ++ci) {
       if (lane < kFeat) {
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
+        for (int q = 0; q < 3; ++q)
 #pragma unroll
-          for (int j = 0; j < kWin; ++j) {
+          for (int j = 0; j < kWin; ++j)
             Fs[(q * 10 + j) * kRsPitch + lane] = __ldg(fst[q] + ((long long)j * cwv[q] + ci) * kFeat + lane);
-            Ws[(q * 10 + j) * kRsPitch + lane] = __ldg(wst[q] + j * kRowW + ci * kFeat + lane);
-          }
-        }
       }
       __syncwarp();
       if (lane < 30) {
         const double* fr = Fs + lane * kRsPitch;
-        const double* wr = Ws + lane * kRsPitch;
+        const double* wr = wrow + ci * kFeat;
 #pragma unroll
         for (int f = 0; f < kFeat; ++f) acc = dadd(acc, dmul(fr[f], wr[f]));  // detector.cpp:84
       }
@@ -107,9 +117,8 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __res
     const bool active = g < 3 && i < n;
     if (!active || lane != 10 * g) continue;
     const Candidate c = cand[i];
-    const int s = c.slot_r >> 3, r = c.slot_r & 7;
-    const LevelDesc& D = P->lv[s];
-    const double sc = dadd(total, bias[r]);
+    const LevelDesc& D = P->lv[c.slot_r >> 3];
+    const double sc = dadd(total, br);
     if (sc > thr) {  // detector.cpp:110 (strict)
       DevDet d;
       d.x = round_half_up(ddiv((double)(c.cx * cell_px), D.c));
@@ -131,14 +140,19 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __res
 void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, const double* w64,
                     const double* bias, double thr, int cell_px, const Candidate* cand,
                     const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
-                    int* det_count, long long cap_pf, int* overflow, int blocks) {
+                    int* det_count, long long cap_pf, int* overflow) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRsSmem);
     attr = true;
   }
-  k_rescore<<<blocks, 32 * kRsWarps, kRsSmem, L.st>>>(Pd, feat64, w64, bias, thr, cell_px, cand, n_cand, cand_cap,
-                                      dets, det_count, cap_pf, overflow);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // per filter: enough CTAs that the five lists together fill every SM twice over
+  const dim3 grid((unsigned)std::max(1, sms * 2 / kFilters + 1), kFilters);
+  k_rescore<<<grid, 32 * kRsWarps, kRsSmem, L.st>>>(Pd, feat64, w64, bias, thr, cell_px, cand, n_cand, cand_cap,
+                                                    dets, det_count, cap_pf, overflow);
   ++*L.counter;
 }
 

@@ -98,6 +98,37 @@ struct Candidate {
   int cx, cy;
 };
 
+// Candidates are appended to one list per filter r (cand + r * cap, count n_cand[r]) so the
+// exact re-score can keep that filter's weights resident.  Warp-aggregated append of this
+// lane's candidate (frame, slot, cx, cy) for every filter whose bit is set in `flags`; all 32
+// lanes must call it.
+__device__ __forceinline__ void emit_candidates(unsigned flags, int frame, int slot, int cx, int cy,
+                                                Candidate* __restrict__ cand, unsigned long long* __restrict__ n_cand,
+                                                long long cap) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < kFilters; ++r) {
+    const bool mine = (flags >> r) & 1u;
+    const unsigned ballot = __ballot_sync(0xffffffffu, mine);
+    if (!ballot) continue;
+    const int leader = __ffs(ballot) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(n_cand + r, (unsigned long long)__popc(ballot));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (mine) {
+      const long long pos = (long long)base + __popc(ballot & ((1u << lane) - 1u));
+      if (pos < cap) {
+        Candidate c;
+        c.frame = frame;
+        c.slot_r = slot * 8 + r;
+        c.cx = cx;
+        c.cy = cy;
+        cand[r * cap + pos] = c;
+      }
+    }
+  }
+}
+
 // Raw detection record on the device (same layout as bl_detection).
 struct DevDet {
   int x, y, w, h;
@@ -174,7 +205,7 @@ void launch_screen_tc(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, c
 void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, const double* w64,
                     const double* bias, double thr, int cell_px, const Candidate* cand,
                     const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
-                    int* det_count, long long cap_pf, int* overflow, int blocks);
+                    int* det_count, long long cap_pf, int* overflow);
 void launch_score_exact_all(const Launch& L, const double* feat64, int cw, int ch, const double* w64,
                             double bias, double* scores);
 size_t nms_key_bytes();

@@ -305,39 +305,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_screen_tc(const PlanDesc* __r
           for (int r = 0; r < kFilters; ++r) dbg_scores[((long long)r * D.sh + cy) * D.sw + cx] = v[r];
         }
         unsigned flags = 0;
-        int cnt = 0;
 #pragma unroll
         for (int r = 0; r < kFilters; ++r)
-          if (ok && v[r] > cutv[r]) {
-            flags |= 1u << r;
-            ++cnt;
-          }
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int tt = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += tt;
-        }
-        const int wtot = __shfl_sync(0xffffffffu, incl, 31);
-        if (wtot > 0) {
-          unsigned long long base = 0;
-          if (lane == 31) base = atomicAdd(n_cand, (unsigned long long)wtot);
-          base = __shfl_sync(0xffffffffu, base, 31);
-          long long pos = (long long)base + incl - cnt;
-          while (flags) {
-            const int r = __ffs(flags) - 1;
-            flags &= flags - 1;
-            if (pos < cap) {
-              Candidate c;
-              c.frame = f;
-              c.slot_r = s * 8 + r;
-              c.cx = cx;
-              c.cy = cy;
-              cand[pos] = c;
-            }
-            ++pos;
-          }
-        }
+          if (ok && v[r] > cutv[r]) flags |= 1u << r;
+        emit_candidates(flags, f, s, cx, cy, cand, n_cand, cap);
       }
       tc_fence_before();
       __syncwarp();
