@@ -357,7 +357,7 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
   H.cells_per_frame = n ? cells / n : 0;
   P.f32_elems = f32;
   P.cap_pf = std::max<long long>(1, anchors_pf * kFilters);
-  P.cand_cap = std::max<long long>(1, (long long)n * anchors_pf);  // per filter list
+  P.cand_cap = std::max<long long>(1, (long long)n * anchors_pf);  // one per anchor (filter mask)
   P.gkeys_pf = nms_gkeys_per_frame(P.cap_pf);
 
   TRY(P.desc.ensure(sizeof(PlanDesc)));
@@ -375,8 +375,8 @@ int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
     TRY(P.feat_tc.ensure(sizeof(float) * std::max<long long>(1, ftc), true));
     if (!regrow) CK(cudaMemset(P.feat_tc.p, 0, sizeof(float) * std::max<long long>(1, ftc)));
   }
-  TRY(P.cand.ensure(sizeof(Candidate) * P.cand_cap * kFilters));
-  TRY(P.n_cand.ensure(sizeof(unsigned long long) * kFilters));
+  TRY(P.cand.ensure(sizeof(Candidate) * P.cand_cap));
+  TRY(P.n_cand.ensure(sizeof(unsigned long long)));
   TRY(P.dets.ensure(sizeof(DevDet) * n * P.cap_pf));
   TRY(P.kept.ensure(sizeof(DevDet) * n * P.cap_pf));
   TRY(P.det_count.ensure(sizeof(int) * n));
@@ -428,7 +428,7 @@ int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long lon
   stage_mark(c, BL_STAGE_GRADHIST);
   const PlanDesc* Pd = P.desc.as<PlanDesc>();
   const int ns = P.host.n_scored;
-  CK(cudaMemsetAsync(P.n_cand.p, 0, sizeof(unsigned long long) * kFilters, c->st));
+  CK(cudaMemsetAsync(P.n_cand.p, 0, sizeof(unsigned long long), c->st));
   CK(cudaMemsetAsync(P.det_count.p, 0, sizeof(int) * n, c->st));
   CK(cudaMemsetAsync(P.overflow.p, 0, sizeof(int), c->st));
   if (ns > 0) {
@@ -1462,12 +1462,12 @@ int bl_debug_screen_tc(bl_ctx* c, const double* features, int cw, int ch, float*
   const long long na = (long long)Lv.sw * Lv.sh;
   TRY(c->s_a.ensure(sizeof(float) * nfl));
   TRY(c->s_b.ensure(sizeof(float) * kFilters * na));
-  TRY(c->s_c.ensure(sizeof(Candidate) * kFilters * na + sizeof(unsigned long long) * kFilters));
+  TRY(c->s_c.ensure(sizeof(Candidate) * na + sizeof(unsigned long long)));
   TRY(c->s_desc.ensure(sizeof(PlanDesc)));
   CK(cudaMemcpyAsync(c->s_a.p, host.data(), sizeof(float) * nfl, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->s_desc.p, &H, sizeof H, cudaMemcpyHostToDevice, c->st));
-  unsigned long long* nc = reinterpret_cast<unsigned long long*>(c->s_c.as<Candidate>() + kFilters * na);
-  CK(cudaMemsetAsync(nc, 0, sizeof(unsigned long long) * kFilters, c->st));
+  unsigned long long* nc = reinterpret_cast<unsigned long long*>(c->s_c.as<Candidate>() + na);
+  CK(cudaMemsetAsync(nc, 0, sizeof(unsigned long long), c->st));
   launch_screen_tc(launch_of(c), H, c->s_desc.as<PlanDesc>(), c->s_a.as<float>(), c->det.w_tc.as<float>(),
                    c->det.cuttc.as<float>(), c->s_c.as<Candidate>(), nc, na, c->s_b.as<float>());
   if (delta)

@@ -38,57 +38,63 @@ BL_DEV double exact_window_score3(const double* __restrict__ feat, int cw, int c
 
 BL_DEV int round_half_up(double v) { return (int)floor(dadd(v, 0.5)); }  // detector.cpp:41
 
-// The re-score proper.  blockIdx.y = filter r: the CTA keeps W_r (fp64, rows padded to 311
-// doubles so the ten window rows sit on distinct banks) resident in shared memory and walks
-// that filter's candidate list.  A warp scores three candidates; lanes 10g + j (g < 3) own
-// window row j of candidate g and run its 310-term dot product strictly in the reference's
-// order.  The feature strips are staged one window cell (31 features) at a time into padded
-// shared memory with coalesced loads -- lane f of the warp fetches feature f of each of the
-// 30 (candidate, row) strips -- instead of one 8-B scalar per lane per term.
+// The re-score proper.  A candidate is an anchor plus the mask of filters whose screen sum
+// passed the cut.  Each CTA keeps all five filters' fp64 weights resident in shared memory
+// (rows padded to 311 doubles so the ten window rows of a filter sit on distinct banks).  A
+// warp scores three anchors; lanes 10g + j (g < 3) own window row j of anchor g.  The
+// feature strips are staged one window cell (31 features) at a time into padded shared
+// memory with coalesced loads (lane f fetches feature f of each of the 30 (anchor, row)
+// strips), copied once into registers, and dotted with every masked filter's row: each
+// filter's 310-term sum runs strictly in the reference's order (detector.cpp:77-88), and
+// the strips cross L1 once per anchor rather than once per (anchor, filter).
 constexpr int kRsPitch = 33;
 constexpr int kRsWPitch = kRowW + 1;  // 311
 constexpr int kRsWarps = 8;
 constexpr int kRsWarpDoubles = 30 * kRsPitch;
-constexpr size_t kRsSmem = sizeof(double) * ((size_t)kRsWarps * kRsWarpDoubles + (size_t)kWin * kRsWPitch);
+constexpr size_t kRsSmem =
+    sizeof(double) * ((size_t)kRsWarps * kRsWarpDoubles + (size_t)kFilters * kWin * kRsWPitch);
 
 __global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __restrict__ P,
                                                  const double* __restrict__ feat64,
                                                  const double* __restrict__ w64,
                                                  const double* __restrict__ bias, double thr,
-                                                 int cell_px, const Candidate* __restrict__ cand_all,
+                                                 int cell_px, const Candidate* __restrict__ cand,
                                                  const unsigned long long* __restrict__ n_cand,
                                                  long long cand_cap, DevDet* __restrict__ dets,
                                                  int* __restrict__ det_count, long long cap_pf,
                                                  int* __restrict__ overflow) {
   extern __shared__ double rs_smem[];
-  const int r = blockIdx.y;
-  const long long n = min((long long)n_cand[r], cand_cap);
+  const long long n = min((long long)*n_cand, cand_cap);
   if (n == 0) return;
-  const Candidate* __restrict__ cand = cand_all + r * cand_cap;
-  double* Wsm = rs_smem + (size_t)kRsWarps * kRsWarpDoubles;  // [10][311]
-  for (int e = threadIdx.x; e < kFilterW; e += blockDim.x) {
-    const int j = e / kRowW;
-    Wsm[j * kRsWPitch + (e - j * kRowW)] = __ldg(w64 + (size_t)r * kFilterW + e);
+  double* Wsm = rs_smem + (size_t)kRsWarps * kRsWarpDoubles;  // [5][10][311]
+  for (int e = threadIdx.x; e < kFilters * kFilterW; e += blockDim.x) {
+    const int rj = e / kRowW;  // r * 10 + j
+    Wsm[rj * kRsWPitch + (e - rj * kRowW)] = __ldg(w64 + e);
   }
   __syncthreads();
-  const double br = bias[r];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* Fs = rs_smem + warp * kRsWarpDoubles;
   const int g = lane / 10;
   const int jl = lane - 10 * g;  // this lane's window row (lanes < 30)
   const long long nw = (long long)gridDim.x * kRsWarps;
   for (long long i0 = ((long long)blockIdx.x * kRsWarps + warp) * 3; i0 < n; i0 += nw * 3) {
-    // strip bases of the three candidates (row 0 of the window, cell 0): every lane holds all
     const double* fst[3];
     int cwv[3];
+    unsigned mask_any = 0, my_mask = 0;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
+      const bool real = i0 + q < n;
       const Candidate c = cand[min(i0 + q, n - 1)];
-      const LevelDesc& D = P->lv[c.slot_r >> 3];
+      const LevelDesc& D = P->lv[c.slot_r >> 8];
       cwv[q] = D.cw;
       fst[q] = feat64 + (D.cell_off + (long long)c.frame * D.cw * D.ch + (long long)c.cy * D.cw + c.cx) * kFeat;
+      const unsigned m = real ? (unsigned)(c.slot_r & 0x1f) : 0u;
+      mask_any |= m;
+      if (g == q) my_mask = m;
     }
-    double acc = 0.0;
+    double acc[kFilters];
+#pragma unroll
+    for (int r = 0; r < kFilters; ++r) acc[r] = 0.0;
     const double* wrow = Wsm + (lane < 30 ? jl : 0) * kRsWPitch;
 #pragma unroll 1
     for (int ci = 0; ci < kWin; ++ci) {
@@ -101,38 +107,49 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __res
       }
       __syncwarp();
       if (lane < 30) {
-        const double* fr = Fs + lane * kRsPitch;
-        const double* wr = wrow + ci * kFeat;
+        double fr[kFeat];
 #pragma unroll
-        for (int f = 0; f < kFeat; ++f) acc = dadd(acc, dmul(fr[f], wr[f]));  // detector.cpp:84
+        for (int f = 0; f < kFeat; ++f) fr[f] = Fs[lane * kRsPitch + f];
+#pragma unroll
+        for (int r = 0; r < kFilters; ++r) {
+          if (!((mask_any >> r) & 1u)) continue;  // warp-uniform
+          const double* wr = wrow + r * kWin * kRsWPitch + ci * kFeat;
+          double a = acc[r];
+#pragma unroll
+          for (int f = 0; f < kFeat; ++f) a = dadd(a, dmul(fr[f], wr[f]));  // detector.cpp:84
+          acc[r] = a;
+        }
       }
       __syncwarp();
     }
-    // column pass (detector.cpp:91-95): the ten row sums in order, then + bias
+    // column pass (detector.cpp:91-95): the ten row sums in order, then + bias, per filter
     const int base = (g < 3 ? g : 0) * 10;
-    double total = 0.0;
 #pragma unroll
-    for (int jj = 0; jj < kWin; ++jj) total = dadd(total, __shfl_sync(0xffffffffu, acc, base + jj));
-    const long long i = i0 + (g < 3 ? g : 0);
-    const bool active = g < 3 && i < n;
-    if (!active || lane != 10 * g) continue;
-    const Candidate c = cand[i];
-    const LevelDesc& D = P->lv[c.slot_r >> 3];
-    const double sc = dadd(total, br);
-    if (sc > thr) {  // detector.cpp:110 (strict)
-      DevDet d;
-      d.x = round_half_up(ddiv((double)(c.cx * cell_px), D.c));
-      d.y = round_half_up(ddiv((double)(c.cy * cell_px), D.c));
-      d.w = D.side;
-      d.h = D.side;
-      d.score = sc;
-      d.scale_index = D.level;
-      d.rotation_index = r;
-      const int idx = atomicAdd(det_count + c.frame, 1);
-      if (idx < cap_pf)
-        dets[(long long)c.frame * cap_pf + idx] = d;
-      else
-        atomicExch(overflow, 1);
+    for (int r = 0; r < kFilters; ++r) {
+      if (!((mask_any >> r) & 1u)) continue;
+      double total = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < kWin; ++jj) total = dadd(total, __shfl_sync(0xffffffffu, acc[r], base + jj));
+      const long long i = i0 + (g < 3 ? g : 0);
+      if (!(g < 3 && i < n && lane == 10 * g && ((my_mask >> r) & 1u))) continue;
+      const Candidate c = cand[i];
+      const LevelDesc& D = P->lv[c.slot_r >> 8];
+      const double sc = dadd(total, bias[r]);
+      if (sc > thr) {  // detector.cpp:110 (strict)
+        DevDet d;
+        d.x = round_half_up(ddiv((double)(c.cx * cell_px), D.c));
+        d.y = round_half_up(ddiv((double)(c.cy * cell_px), D.c));
+        d.w = D.side;
+        d.h = D.side;
+        d.score = sc;
+        d.scale_index = D.level;
+        d.rotation_index = r;
+        const int idx = atomicAdd(det_count + c.frame, 1);
+        if (idx < cap_pf)
+          dets[(long long)c.frame * cap_pf + idx] = d;
+        else
+          atomicExch(overflow, 1);
+      }
     }
   }
 }
@@ -149,8 +166,7 @@ void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, c
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // per filter: enough CTAs that the five lists together fill every SM twice over
-  const dim3 grid((unsigned)std::max(1, sms * 2 / kFilters + 1), kFilters);
+  const dim3 grid((unsigned)sms);  // persistent: one CTA per SM (the weights fill most of its smem)
   k_rescore<<<grid, 32 * kRsWarps, kRsSmem, L.st>>>(Pd, feat64, w64, bias, thr, cell_px, cand, n_cand, cand_cap,
                                                     dets, det_count, cap_pf, overflow);
   ++*L.counter;

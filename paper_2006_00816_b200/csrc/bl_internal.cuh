@@ -91,40 +91,37 @@ BL_HD_INLINE int find_level(const LevelBegins& B, long long id) {
   return s;
 }
 
-// Candidate from the fp32 screen: (frame, scored-level slot, filter, cx, cy).
+// Candidate from the screen: (frame, scored-level slot, filter mask, cx, cy).
 struct Candidate {
   int frame;
-  int slot_r;   // slot * 8 + r
+  int slot_r;   // (slot << 8) | mask of the filters that passed the screen
   int cx, cy;
 };
 
-// Candidates are appended to one list per filter r (cand + r * cap, count n_cand[r]) so the
-// exact re-score can keep that filter's weights resident.  Warp-aggregated append of this
-// lane's candidate (frame, slot, cx, cy) for every filter whose bit is set in `flags`; all 32
-// lanes must call it.
+// One candidate per screened ANCHOR: slot_r = slot * 8 + r is replaced by (slot << 8) | mask,
+// mask = the filters whose screen sum passed the cut, so the exact re-score stages the
+// anchor's feature strips once for all of them.  Warp-aggregated append; all 32 lanes must
+// call it (flags == 0: no candidate).
 __device__ __forceinline__ void emit_candidates(unsigned flags, int frame, int slot, int cx, int cy,
                                                 Candidate* __restrict__ cand, unsigned long long* __restrict__ n_cand,
                                                 long long cap) {
   const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int r = 0; r < kFilters; ++r) {
-    const bool mine = (flags >> r) & 1u;
-    const unsigned ballot = __ballot_sync(0xffffffffu, mine);
-    if (!ballot) continue;
-    const int leader = __ffs(ballot) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(n_cand + r, (unsigned long long)__popc(ballot));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (mine) {
-      const long long pos = (long long)base + __popc(ballot & ((1u << lane) - 1u));
-      if (pos < cap) {
-        Candidate c;
-        c.frame = frame;
-        c.slot_r = slot * 8 + r;
-        c.cx = cx;
-        c.cy = cy;
-        cand[r * cap + pos] = c;
-      }
+  const bool mine = flags != 0;
+  const unsigned ballot = __ballot_sync(0xffffffffu, mine);
+  if (!ballot) return;
+  const int leader = __ffs(ballot) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(n_cand, (unsigned long long)__popc(ballot));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (mine) {
+    const long long pos = (long long)base + __popc(ballot & ((1u << lane) - 1u));
+    if (pos < cap) {
+      Candidate c;
+      c.frame = frame;
+      c.slot_r = (slot << 8) | (int)flags;
+      c.cx = cx;
+      c.cy = cy;
+      cand[pos] = c;
     }
   }
 }
