@@ -855,7 +855,11 @@ int bl_ctx_create(int device, bl_ctx** out) {
   c->device = device;
   CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->hst, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&c->est, cudaStreamNonBlocking));
+  {  // the cascade fills the gaps of the next batch's detection: lowest priority
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c->est, cudaStreamNonBlocking, lo));
+  }
   c->st = c->own;
   for (Slot& S : c->slots) {
     CK(cudaStreamCreateWithFlags(&S.d2h, cudaStreamNonBlocking));
