@@ -2,7 +2,7 @@
 """bench.py -- frames/sec of detect + 68 landmarks @640x480 on B200 (BASELINE.json metric).
 
 Workload (one step, per GPU): B synthetic 640x480 eyeblink-camera frames (u8, seeded ring
-targets) -> pyramid -> gradHist -> features -> fp32 screen -> exact fp64 re-score ->
+targets) -> pyramid -> gradHist -> features -> tcgen05 tf32 screen -> exact fp64 re-score ->
 threshold -> NMS -> ERT 15 x 500 x depth-4 random-init 68-landmark cascade on every kept
 detection.  Models: the reference's own ring-pattern detector (tests/golden/
 pattern_detector.npz, exported from the reference's pattern_detector()) and a seeded
@@ -144,8 +144,8 @@ def algorithmic_bytes_per_frame():
     return {
         "pyramid": res,
         "gradhist": px + cells * 19 * 8,                  # level pixels read, bins + energy written
-        "features": cells * (19 * 8 + 31 * 8 + 31 * 4),  # bins+energy read, fp64 + fp32 features written
-        "screen": cells * 31 * 4,                         # fp32 feature planes read once
+        "features": cells * (19 * 8 + 31 * 8 + 32 * 4),  # bins+energy read, fp64 + tf32 planes written
+        "screen": cells * 32 * 4,                         # tf32 feature planes read once
         "anchors": anchors,
         "cells": cells,
     }

@@ -95,7 +95,7 @@ int bl_ctx_launch_count(bl_ctx* ctx, uint64_t* out);
 /* Per-stage CUDA-event timing of subsequent pipeline calls (adds events; off by default). */
 int bl_ctx_enable_stage_timing(bl_ctx* ctx, int enable);
 int bl_ctx_stage_times(bl_ctx* ctx, float* ms /* BL_STAGE_COUNT */, int* launches /* BL_STAGE_COUNT */);
-/* Capture each (geometry, batch) pipeline into a CUDA graph and replay it (default on). */
+/* Reserved (accepted, currently no effect): the pipeline is enqueued as individual launches. */
 int bl_ctx_enable_graphs(bl_ctx* ctx, int enable);
 /* Classifier screen implementation (both feed the same exact fp64 re-score, so detections
  * are bit-identical either way): BL_SCREEN_TCGEN05 -- implicit GEMM on the tensor cores
