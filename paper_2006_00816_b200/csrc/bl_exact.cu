@@ -216,12 +216,33 @@ BL_DEV double iou_exact(const DevDet& a, const DevDet& b) {
   return ddiv(inter, uni);
 }
 
+// iou(a, b) > thr with the reference's rounding (detector.cpp:16-28, 134), deciding in fp32
+// when the quotient is clearly away from thr (|fp32 quotient - exact| < 1e-6 for integer
+// areas) and falling back to the exact fp64 quotient otherwise.
+BL_DEV bool iou_exceeds(const DevDet& a, const DevDet& b, double thr) {
+  const long long ix0 = max(a.x, b.x);
+  const long long iy0 = max(a.y, b.y);
+  const long long ix1 = min((long long)(a.x + a.w), (long long)(b.x + b.w));
+  const long long iy1 = min((long long)(a.y + a.h), (long long)(b.y + b.h));
+  const long long iw = ix1 - ix0;
+  const long long ih = iy1 - iy0;
+  if (iw <= 0 || ih <= 0) return 0.0 > thr;
+  const long long uni = (long long)a.w * a.h + (long long)b.w * b.h - iw * ih;
+  if (uni <= 0) return iou_exact(a, b) > thr;
+  const float q = __fdividef((float)(iw * ih), (float)uni);
+  const float t = (float)thr;
+  if (q > t + 1e-5f) return true;
+  if (q < t - 1e-5f) return false;
+  return iou_exact(a, b) > thr;
+}
+
 struct NmsKey {
   double score;
   unsigned long long t1, t2;  // (y, x) and (scale, rotation), sign-flipped for unsigned order
   int idx;
   int pad;
 };
+static_assert(sizeof(NmsKey) == sizeof(DevDet), "sorted detections reuse the key slots");
 
 // detector.cpp:125-129: score descending, then (y, x, scale_index, rotation_index) ascending.
 BL_DEV bool before(const NmsKey& a, const NmsKey& b) {
@@ -235,8 +256,8 @@ BL_DEV unsigned long long pack2(int hi, int lo) {
   return ((unsigned long long)((unsigned)hi ^ 0x80000000u) << 32) | (unsigned)(lo ^ 0x80000000);
 }
 
-constexpr int kNmsSmemKeys = 2048;   // keys sorted in shared memory up to this count
-constexpr int kNmsSmemKept = 1024;   // kept boxes cached in shared memory
+constexpr int kNmsSmemKeys = 512;    // keys sorted in shared memory up to this count
+constexpr int kNmsSmemKept = 256;    // kept boxes cached in shared memory
 
 // One CTA per frame: bitonic sort of the frame's detections, then the greedy scan by
 // warp 0 (kept boxes checked 32 at a time with __any_sync).
@@ -290,16 +311,73 @@ __global__ void __launch_bounds__(256) k_nms(const DevDet* __restrict__ dets,
       __syncthreads();
     }
   }
+  // gather the detections in sorted order next to the SM (in place of their keys when those
+  // live in shared memory: same 32-B size, each thread reads its own key before overwriting
+  // it), so the serial greedy scan below reads shared memory, not scattered global lines
+  const bool smem_sorted = Pn <= kNmsSmemKeys;
+  DevDet* sorted = reinterpret_cast<DevDet*>(keys);
+  if (smem_sorted) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int idx = keys[i].idx;
+      sorted[i] = D[idx];
+    }
+    __syncthreads();
+  }
+  DevDet* out = kept_out + (long long)f * cap_pf;
+  if (smem_sorted) {
+    // Warp-batched form of the greedy scan (detector.cpp:130-140): 32 boxes of the order at a
+    // time.  Each lane tests its box against every box kept so far and against the earlier
+    // boxes of its batch; the batch is then resolved in order with bit operations (box j is
+    // kept iff no kept box suppresses it and no earlier KEPT box of the batch overlaps it) --
+    // exactly the sequential scan's decisions, in its order.
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    int kept = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const bool valid = i < n;
+      const DevDet d = sorted[valid ? i : n - 1];
+      bool sup = !valid;
+      for (int k = 0; k < kept && !sup; ++k) {
+        const DevDet kb = k < kNmsSmemKept ? kept_s[k] : out[k];
+        if (iou_exceeds(d, kb, iou_thr)) sup = true;
+      }
+      uint32_t ovl = 0;  // bit j: earlier batch box j overlaps this box
+#pragma unroll 4
+      for (int jj = 0; jj < 31; ++jj) {
+        DevDet o;
+        o.x = __shfl_sync(0xffffffffu, d.x, jj);
+        o.y = __shfl_sync(0xffffffffu, d.y, jj);
+        o.w = __shfl_sync(0xffffffffu, d.w, jj);
+        o.h = __shfl_sync(0xffffffffu, d.h, jj);
+        if (jj < lane && iou_exceeds(d, o, iou_thr)) ovl |= 1u << jj;
+      }
+      const uint32_t alive = __ballot_sync(0xffffffffu, !sup);
+      uint32_t keep = 0;
+      for (int jj = 0; jj < 32; ++jj) {
+        const uint32_t oj = __shfl_sync(0xffffffffu, ovl, jj);
+        if (((alive >> jj) & 1u) && !(oj & keep)) keep |= 1u << jj;
+      }
+      if ((keep >> lane) & 1u) {
+        const int pos = kept + __popc(keep & ((1u << lane) - 1u));
+        out[pos] = d;
+        if (pos < kNmsSmemKept) kept_s[pos] = d;
+      }
+      kept += __popc(keep);
+      __syncwarp();
+    }
+    if (lane == 0) kept_count[f] = kept;
+    return;
+  }
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
-  DevDet* out = kept_out + (long long)f * cap_pf;
   int kept = 0;
   for (int i = 0; i < n; ++i) {
-    const DevDet d = D[keys[i].idx];
+    const DevDet d = smem_sorted ? sorted[i] : D[keys[i].idx];
     bool sup = false;
     for (int k = lane; k < kept; k += 32) {
       const DevDet kb = k < kNmsSmemKept ? kept_s[k] : out[k];
-      if (iou_exact(d, kb) > iou_thr) sup = true;  // detector.cpp:134
+      if (iou_exceeds(d, kb, iou_thr)) sup = true;  // detector.cpp:134
     }
     if (!__any_sync(0xffffffffu, sup)) {
       if (lane == 0) {
