@@ -210,6 +210,7 @@ struct bl_ctx {
   uint64_t next_ticket = 1;
   int face_cap_per_frame = 64;  // device-side capacity of landmarked faces per frame
   int screen = BL_SCREEN_TCGEN05;
+  bool ert_fused = true;  // BL_ERT=levels selects the per-level kernels (experiments)
 };
 
 namespace {
@@ -526,6 +527,11 @@ int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix
     leaf = wk.leafs.as<uint8_t>();
   }
   CK(cudaMemsetAsync(err_dev, 0, sizeof(int), st));
+  if (c->ert_fused && ert_cascade_fits(E.dev)) {  // one launch for the whole cascade
+    launch_ert_cascade(L, E.dev, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
+                       n_faces_dev, nf, out_xy, leaf_dev, (long long)E.dev.T * E.dev.K, err_dev);
+    return BL_OK;
+  }
   launch_ert_init(L, E.dev, n_faces_dev, nf, wk.cur.as<double>());
   for (int t = 0; t < E.dev.T; ++t)
     launch_ert_level(L, E.dev, t, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
@@ -879,6 +885,7 @@ int bl_ctx_create(int device, bl_ctx** out) {
   }
   set_direction_table(ux, uy);
   if (const char* e = std::getenv("BL_SCREEN")) c->screen = std::strcmp(e, "fp32") == 0 ? BL_SCREEN_FP32 : BL_SCREEN_TCGEN05;
+  if (const char* e = std::getenv("BL_ERT")) c->ert_fused = std::strcmp(e, "levels") != 0;
   CK(cudaGetLastError());
   *out = c.release();
   return BL_OK;

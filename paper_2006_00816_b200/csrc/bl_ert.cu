@@ -52,6 +52,8 @@ BL_DEV double sample_px(const void* fr, int w, int h, long long pitch, int bx, i
   return __ldg((const double*)fr + (long long)iy * pitch + ix);
 }
 
+__device__ int face_transform(const ErtDev& M, const double* c, double& A, double& B);
+
 // (1) similarity_transform(current, mean) per face, ert.cpp:26-69.  A warp per face stages
 // the current shape in shared memory; lane 0 then runs the sums sequentially in the
 // reference's order (bit-identical), then CUDA hypot/atan2/cos/sin.  Stores the linear part
@@ -72,7 +74,17 @@ __global__ void __launch_bounds__(32 * kXfFaces) k_ert_xform(ErtDev M, const int
   for (int i = lane; i < L2; i += 32) sc[warp][i] = cur[i];
   __syncwarp();
   if (lane != 0) return;
-  const double* c = sc[warp];
+  double A = 0.0, B = 0.0;
+  const int e = face_transform(M, sc[warp], A, B);
+  if (e) atomicExch(err, e);
+  tf[face] = make_double2(A, B);
+}
+
+// similarity_transform(current -> mean) of one face (ert.cpp:26-69), sequential sums in the
+// reference's order; returns 0 or the reference's error (1: source shape has no spread, 2:
+// target shape has no spread) and the linear part (scale*cos, scale*sin) in A, B.
+__device__ int face_transform(const ErtDev& M, const double* c, double& A, double& B) {
+  const int L = M.L;
   double mfx = 0.0, mfy = 0.0;
   for (int i = 0; i < L; ++i) {
     mfx = dadd(mfx, c[2 * i]);
@@ -90,21 +102,16 @@ __global__ void __launch_bounds__(32 * kXfFaces) k_ert_xform(ErtDev M, const int
     sre = dadd(sre, dadd(dmul(fx, txp), dmul(fy, typ)));
     sim = dadd(sim, dsub(dmul(fx, typ), dmul(fy, txp)));
   }
-  double A = 0.0, B = 0.0;
-  if (!(sff > 0.0)) {
-    atomicExch(err, 1);  // "source shape has no spread" (ert.cpp:56-57)
-  } else {
-    const double a = ddiv(sre, sff), b = ddiv(sim, sff);
-    const double scale = hypot(a, b);
-    if (!(scale > 0.0)) {
-      atomicExch(err, 2);  // "target shape has no spread" (ert.cpp:62-63)
-    } else {
-      const double rot = atan2(b, a);
-      A = dmul(scale, cos(rot));
-      B = dmul(scale, sin(rot));
-    }
-  }
-  tf[face] = make_double2(A, B);
+  A = 0.0;
+  B = 0.0;
+  if (!(sff > 0.0)) return 1;  // "source shape has no spread" (ert.cpp:56-57)
+  const double a = ddiv(sre, sff), b = ddiv(sim, sff);
+  const double scale = hypot(a, b);
+  if (!(scale > 0.0)) return 2;  // "target shape has no spread" (ert.cpp:62-63)
+  const double rot = atan2(b, a);
+  A = dmul(scale, cos(rot));
+  B = dmul(scale, sin(rot));
+  return 0;
 }
 
 // (2) one CTA per face, one thread per tree: traverse_tree (ert.cpp:87-97) with
@@ -210,6 +217,141 @@ void launch_ert_level(const Launch& L, const ErtDev& M, int t, const void* frame
   k_ert_accum<<<(unsigned)div_up((long long)cap * M.L, 256), 256, 0, L.st>>>(M, t, n_faces, cap, cur, leaf_idx,
                                                                            leaf_stride);
   *L.counter += 3;
+}
+
+// The whole cascade for a group of faces in ONE launch (ert.cpp:99-136).  Faces are
+// independent, so a CTA owns kFcFaces faces and runs every level itself, with block barriers
+// between the level's three phases -- the same arithmetic as k_ert_xform / k_ert_traverse /
+// k_ert_accum (bit-identical), without 3 x T launches and the inter-kernel gaps:
+//   xform    warp per face: similarity transform of the staged current shape;
+//   traverse thread per (face, tree): level-order descent, leaf index -> smem;
+//   accum    thread per (face, landmark pair): the K selected leaf rows in tree order.
+// Current shapes, transforms and the level's leaf indices live in shared memory.
+#ifndef BL_ERT_FACES
+#define BL_ERT_FACES 4
+#endif
+constexpr int kFcFaces = BL_ERT_FACES;
+constexpr int kFcThreads = ((kFcFaces * 68 + 31) / 32) * 32;  // one thread per (face, pair) at L = 68
+
+template <bool U8>
+__global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void* __restrict__ frames, int w, int h,
+                                                     long long pitch, long long fstride,
+                                                     const int* __restrict__ face_frame,
+                                                     const int* __restrict__ boxes, int box_stride,
+                                                     const int* __restrict__ n_faces, int cap,
+                                                     double* __restrict__ out_xy, uint8_t* __restrict__ leaf_out,
+                                                     long long leaf_out_stride, int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char fc_smem[];
+  const int L = M.L, L2 = 2 * L, K = M.K, S = M.S, NL = M.NL;
+  double* sc = reinterpret_cast<double*>(fc_smem);                    // [kFcFaces][2L]
+  double2* stf = reinterpret_cast<double2*>(sc + kFcFaces * L2);      // [kFcFaces]
+  uint8_t* sli = reinterpret_cast<uint8_t*>(stf + kFcFaces);          // [kFcFaces][K]
+  const int n = min(*n_faces, cap);
+  const int f0 = blockIdx.x * kFcFaces;
+  if (f0 >= n) return;
+  const int nf = min(kFcFaces, n - f0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < nf * L2; e += blockDim.x) sc[e] = M.mean_xy[e % L2];  // ert.cpp:106
+  __syncthreads();
+  for (int t = 0; t < M.T; ++t) {
+    // (1) transforms
+    if (warp < nf && lane == 0) {
+      double A, B;
+      const int e = face_transform(M, sc + warp * L2, A, B);
+      if (e) atomicExch(err, e);
+      stf[warp] = make_double2(A, B);
+    }
+    __syncthreads();
+    // (2) traversals
+    const SplitRec* lvl = M.split + (long long)t * S * K;
+    for (int e = tid; e < nf * K; e += blockDim.x) {
+      const int fi = e / K, k = e - fi * K;
+      const int face = f0 + fi;
+      const double2 ab = stf[fi];
+      const int* bx = boxes + (long long)face * box_stride;
+      const int X = bx[0], Y = bx[1], W = bx[2], H = bx[3];
+      const void* fr = (const char*)frames + (long long)face_frame[face] * fstride * (U8 ? 1 : 8);
+      const double* cur = sc + fi * L2;
+      int node = 0;
+      while (node < S) {
+        const SplitRec* r = lvl + (long long)node * K + k;
+        const double2 oa = __ldg(reinterpret_cast<const double2*>(r));
+        const double2 ob = __ldg(reinterpret_cast<const double2*>(r) + 1);
+        const int4 tail = __ldg(reinterpret_cast<const int4*>(r) + 2);
+        const double thr = __hiloint2double(tail.y, tail.x);
+        const int an_a = (short)(tail.z & 0xffff), an_b = (short)(tail.z >> 16);
+        const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, cur, ab.x, ab.y, an_a, oa.x, oa.y);
+        const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, cur, ab.x, ab.y, an_b, ob.x, ob.y);
+        node = dsub(ia, ib) > thr ? 2 * node + 1 : 2 * node + 2;  // ert.cpp:87-97
+      }
+      sli[fi * K + k] = (uint8_t)(node - S);
+      if (leaf_out) leaf_out[(long long)face * leaf_out_stride + (long long)t * K + k] = (uint8_t)(node - S);
+    }
+    __syncthreads();
+    // (3) leaf sums in tree order, cur += shrinkage * delta (ert.cpp:118-126)
+    if (tid < nf * L) {
+      const int fi = tid / L, p = tid - fi * L;
+      const uint8_t* li = sli + fi * K;
+      const double2* lv = reinterpret_cast<const double2*>(M.leaves + (long long)t * K * NL * 2 * L) + p;
+      const int row = NL * L;
+      double ax = 0.0, ay = 0.0;
+      int k = 0;
+      for (; k + 16 <= K; k += 16) {
+        double2 v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = __ldg(lv + (k + u) * row + li[k + u] * L);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          ax = dadd(ax, v[u].x);
+          ay = dadd(ay, v[u].y);
+        }
+      }
+      for (; k < K; ++k) {
+        const double2 v = __ldg(lv + k * row + li[k] * L);
+        ax = dadd(ax, v.x);
+        ay = dadd(ay, v.y);
+      }
+      double* c = sc + fi * L2 + 2 * p;
+      c[0] = dadd(c[0], dmul(M.shrinkage, ax));
+      c[1] = dadd(c[1], dmul(M.shrinkage, ay));
+    }
+    __syncthreads();
+  }
+  // ert.cpp:132-133: box.x + p.x * box.w, box.y + p.y * box.h
+  for (int e = tid; e < nf * L2; e += blockDim.x) {
+    const int fi = e / L2, c = e - fi * L2;
+    const int* b = boxes + (long long)(f0 + fi) * box_stride;
+    out_xy[(long long)(f0 + fi) * L2 + c] = (c & 1) ? dadd((double)b[1], dmul(sc[e], (double)b[3]))
+                                                    : dadd((double)b[0], dmul(sc[e], (double)b[2]));
+  }
+}
+
+bool ert_cascade_fits(const ErtDev& M) {
+  return M.L * kFcFaces <= kFcThreads && 2 * M.L <= kMaxL2;
+}
+
+void launch_ert_cascade(const Launch& L, const ErtDev& M, const void* frames, int u8, int w, int h, long long pitch,
+                        long long fstride, const int* face_frame, const int* boxes, int box_stride,
+                        const int* n_faces, int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride,
+                        int* err) {
+  const size_t smem = sizeof(double) * kFcFaces * 2 * M.L + sizeof(double2) * kFcFaces + (size_t)kFcFaces * M.K;
+  static size_t attr_u8 = 0, attr_f64 = 0;
+  size_t& attr = u8 ? attr_u8 : attr_f64;
+  if (smem > 48 * 1024 && smem > attr) {
+    if (u8)
+      cudaFuncSetAttribute(k_ert_cascade<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else
+      cudaFuncSetAttribute(k_ert_cascade<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  const unsigned grid = (unsigned)div_up(cap, kFcFaces);
+  if (u8)
+    k_ert_cascade<true><<<grid, kFcThreads, smem, L.st>>>(M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride,
+                                                   n_faces, cap, out_xy, leaf_out, leaf_out_stride, err);
+  else
+    k_ert_cascade<false><<<grid, kFcThreads, smem, L.st>>>(M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride,
+                                                    n_faces, cap, out_xy, leaf_out, leaf_out_stride, err);
+  ++*L.counter;
 }
 
 __global__ void k_ert_finish(ErtDev M, const int* __restrict__ boxes, int box_stride,
