@@ -40,7 +40,8 @@ enum {
   BL_ERR_MODEL = 2,    /* model shape/content invalid  -> blinkline::model_error */
   BL_ERR_CUDA = 3,     /* CUDA runtime/device failure   -> std::runtime_error */
   BL_ERR_CAPACITY = 4, /* a fixed device capacity was exceeded -> std::runtime_error */
-  BL_ERR_STATE = 5     /* no model uploaded / context misuse */
+  BL_ERR_STATE = 5,    /* no model uploaded / context misuse */
+  BL_ERR_IO = 6        /* file unreadable / malformed PGM  -> blinkline::io_error */
 };
 
 enum { BL_PIX_U8 = 0, BL_PIX_F64 = 1 };
@@ -200,6 +201,40 @@ int bl_debug_sqrt(bl_ctx* ctx, const double* in, int64_t n, double* fast, double
  * the rigorous per-filter error bound the candidate cut uses in delta[r]. */
 int bl_debug_screen_tc(bl_ctx* ctx, const double* features, int cells_w, int cells_h, float* scores,
                        double* delta);
+
+/* ---------------------------------------------------- data formats (host only) ---- */
+/* Frames.  replaces: load_pgm (image.hpp:25, image.cpp:67-114).  P5 or P2, maxval <= 255,
+ * parsed straight to u8 (exact: PGM samples are integers).  pixels == NULL: header only
+ * (dimensions).  Errors: BL_ERR_IO with the reference's message and byte offset. */
+int bl_read_pgm(const char* path, int* w, int* h, uint8_t* pixels, size_t capacity);
+/* replaces: save_pgm (image.hpp:28, image.cpp:116-127): P5, values clamped and rounded. */
+int bl_write_pgm(const char* path, const double* pixels, int w, int h);
+
+/* Detector model file "hog-v1".  replaces: load_detector_model / save_model
+ * (detector.hpp:99-100, detector.cpp:291-351).  weights: 5 x window_cells^2 x 31 doubles
+ * (filter-major, the bl_detector_upload layout); NULL -> scalars only (call once for
+ * window_cells, again with buffers).  Errors: BL_ERR_IO (cannot open), BL_ERR_MODEL. */
+int bl_read_detector_json(const char* path, double* weights, double* biases, double* threshold,
+                          int* window_cells, int* cell_px, int* scale_num, int* scale_den,
+                          double* min_face_ratio);
+int bl_write_detector_json(const char* path, const double* weights, const double* biases,
+                           double threshold, int window_cells, int cell_px, int scale_num,
+                           int scale_den, double min_face_ratio);
+
+/* ERT model file "ert-v1".  replaces: load_ert_model / save_model (ert.hpp:128-129,
+ * ert.cpp:358-469).  Open parses once into the bl_ert_upload layout (anchors [T][K][S][2],
+ * split_params [T][K][S][5] = ox_a, oy_a, ox_b, oy_b, thr, leaves [T][K][2^F][L][2]); copy
+ * the arrays out, or upload them to a context, then close. */
+typedef struct bl_ert_file bl_ert_file;
+int bl_ert_file_open(const char* path, bl_ert_file** out, int* L, int* T, int* K, int* F,
+                     double* shrinkage);
+int bl_ert_file_copy(const bl_ert_file* file, double* mean_xy, int32_t* anchors, double* split_params,
+                     double* leaves);
+int bl_ert_file_upload(const bl_ert_file* file, bl_ctx* ctx);
+void bl_ert_file_close(bl_ert_file* file);
+int bl_write_ert_json(const char* path, int L, int T, int K, int F, double shrinkage,
+                      const double* mean_xy, const int32_t* anchors, const double* split_params,
+                      const double* leaves);
 
 #ifdef __cplusplus
 }

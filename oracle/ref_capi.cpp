@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <exception>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -28,6 +29,7 @@
 #include <vector>
 
 #include "blinkline/detector.hpp"
+#include "blinkline/errors.hpp"
 #include "blinkline/ert.hpp"
 #include "blinkline/hog.hpp"
 #include "blinkline/image.hpp"
@@ -531,6 +533,135 @@ int ref_landmarks_batch_u8(const uint8_t* frames, int w, int h, const int32_t* f
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;
+  }
+}
+
+// ------------------------------------------------------ file formats (reference I/O) ----
+// 0 ok, 1 io_error, 2 model_error, 3 invalid_argument / other; message via ref_last_error.
+static int io_catch(const std::exception_ptr& ep) {
+  try {
+    std::rethrow_exception(ep);
+  } catch (const io_error& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const model_error& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+int ref_load_pgm(const char* path, int* w, int* h, double* px, long long cap) {
+  try {
+    const GrayImage img = load_pgm(path);
+    *w = img.width;
+    *h = img.height;
+    if (px && cap >= (long long)img.pixels.size()) std::memcpy(px, img.pixels.data(), sizeof(double) * img.pixels.size());
+    return 0;
+  } catch (...) {
+    return io_catch(std::current_exception());
+  }
+}
+
+int ref_save_pgm(const char* path, const double* px, int w, int h) {
+  try {
+    save_pgm(to_image(px, w, h), path);
+    return 0;
+  } catch (...) {
+    return io_catch(std::current_exception());
+  }
+}
+
+int ref_save_detector_json(const char* path, const double* weights, const double* biases, double thr,
+                           int window_cells, int cell_px, int scale_num, int scale_den, double min_face_ratio) {
+  try {
+    save_model(to_model(weights, biases, thr, window_cells, cell_px, scale_num, scale_den, min_face_ratio), path);
+    return 0;
+  } catch (...) {
+    return io_catch(std::current_exception());
+  }
+}
+
+int ref_load_detector_json(const char* path, double* weights, double* biases, double* thr, int* window_cells,
+                           int* cell_px, int* scale_num, int* scale_den, double* min_face_ratio) {
+  try {
+    const DetectorModel m = load_detector_model(path);
+    for (int r = 0; r < 5; ++r) {
+      if (weights) std::memcpy(weights + r * m.filters[r].weights.size(), m.filters[r].weights.data(),
+                               sizeof(double) * m.filters[r].weights.size());
+      biases[r] = m.filters[r].bias;
+    }
+    *thr = m.detection_threshold;
+    *window_cells = m.window_cells;
+    *cell_px = m.cell_px;
+    *scale_num = m.scale_num;
+    *scale_den = m.scale_den;
+    *min_face_ratio = m.min_face_ratio;
+    return 0;
+  } catch (...) {
+    return io_catch(std::current_exception());
+  }
+}
+
+int ref_ert_save_json(void* h, const char* path) {
+  try {
+    save_model(static_cast<RefErt*>(h)->model, path);
+    return 0;
+  } catch (...) {
+    return io_catch(std::current_exception());
+  }
+}
+
+// Loads an ert-v1 file with the reference and exports it in the bl_ert_upload layout.
+// dims[5] = L, T, K, F (and shrinkage in *shrink); arrays may be NULL for a dims-only call.
+int ref_ert_load_json(const char* path, int* dims, double* shrink, double* mean_xy, int32_t* anchors,
+                      double* split_params, double* leaves) {
+  try {
+    const ErtModel m = load_ert_model(path);
+    const int L = m.landmark_count(), T = m.levels(), K = m.trees_per_level();
+    const int F = (T > 0 && K > 0) ? m.cascade[0][0].depth : 0;
+    dims[0] = L;
+    dims[1] = T;
+    dims[2] = K;
+    dims[3] = F;
+    *shrink = m.shrinkage;
+    if (mean_xy)
+      for (int i = 0; i < L; ++i) {
+        mean_xy[2 * i] = m.mean_shape.points[i].x;
+        mean_xy[2 * i + 1] = m.mean_shape.points[i].y;
+      }
+    std::size_t si = 0, li = 0;
+    for (const auto& level : m.cascade)
+      for (const RegressionTree& tree : level) {
+        for (const SplitNode& n : tree.splits) {
+          if (anchors) {
+            anchors[2 * si] = n.anchor_a;
+            anchors[2 * si + 1] = n.anchor_b;
+          }
+          if (split_params) {
+            double* q = split_params + 5 * si;
+            q[0] = n.offset_a.x;
+            q[1] = n.offset_a.y;
+            q[2] = n.offset_b.x;
+            q[3] = n.offset_b.y;
+            q[4] = n.threshold;
+          }
+          ++si;
+        }
+        for (const auto& leaf : tree.leaves) {
+          if (leaves)
+            for (std::size_t i = 0; i < leaf.size(); ++i) {
+              leaves[2 * (li + i)] = leaf[i].x;
+              leaves[2 * (li + i) + 1] = leaf[i].y;
+            }
+          li += leaf.size();
+        }
+      }
+    return 0;
+  } catch (...) {
+    return io_catch(std::current_exception());
   }
 }
 

@@ -33,6 +33,8 @@ __all__ = [
     "build_pyramid", "downscale_bilinear", "compute_gradients", "histogramize", "cell_energy",
     "compute_features", "extract_features", "score_separable", "score_dense", "nms",
     "orientation_bins", "detect_faces", "predict_landmarks", "default_context",
+    "read_pgm", "write_pgm", "read_detector_json", "write_detector_json", "read_ert_json", "write_ert_json",
+    "IoError",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -51,7 +53,7 @@ DET_DTYPE = np.dtype([("x", "<i4"), ("y", "<i4"), ("w", "<i4"), ("h", "<i4"), ("
                       ("scale_index", "<i4"), ("rotation_index", "<i4")], align=True)
 assert DET_DTYPE.itemsize == 32
 
-BL_OK, BL_ERR_INVALID, BL_ERR_MODEL, BL_ERR_CUDA, BL_ERR_CAPACITY, BL_ERR_STATE = range(6)
+BL_OK, BL_ERR_INVALID, BL_ERR_MODEL, BL_ERR_CUDA, BL_ERR_CAPACITY, BL_ERR_STATE, BL_ERR_IO = range(7)
 BL_PIX_U8, BL_PIX_F64 = 0, 1
 SCREEN_TCGEN05, SCREEN_FP32 = 0, 1
 MAX_IN_FLIGHT = 3  # BL_MAX_IN_FLIGHT
@@ -60,6 +62,10 @@ STAGES = ["h2d", "pyramid", "gradhist", "features", "screen", "rescore", "nms", 
 
 class ModelError(RuntimeError):
     """The reference's blinkline::model_error."""
+
+
+class IoError(OSError):
+    """The reference's blinkline::io_error (unreadable file, malformed PGM)."""
 
 
 class CapacityError(RuntimeError):
@@ -107,6 +113,19 @@ _SIGS = {
     "bl_orientation_bins": (C.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "bl_debug_sqrt": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "bl_debug_screen_tc": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp]),
+    "bl_read_pgm": (C.c_int, [C.c_char_p, _P(C.c_int), _P(C.c_int), _vp, _sz]),
+    "bl_write_pgm": (C.c_int, [C.c_char_p, _vp, C.c_int, C.c_int]),
+    "bl_read_detector_json": (C.c_int, [C.c_char_p, _vp, _vp, _P(C.c_double), _P(C.c_int), _P(C.c_int),
+                                        _P(C.c_int), _P(C.c_int), _P(C.c_double)]),
+    "bl_write_detector_json": (C.c_int, [C.c_char_p, _vp, _vp, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_double]),
+    "bl_ert_file_open": (C.c_int, [C.c_char_p, _P(_vp), _P(C.c_int), _P(C.c_int), _P(C.c_int), _P(C.c_int),
+                                   _P(C.c_double)]),
+    "bl_ert_file_copy": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "bl_ert_file_upload": (C.c_int, [_vp, _vp]),
+    "bl_ert_file_close": (None, [_vp]),
+    "bl_write_ert_json": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _vp, _vp, _vp,
+                                    _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)
@@ -124,6 +143,8 @@ def _err(rc, total=None):
         raise ValueError(msg)
     if rc == BL_ERR_MODEL:
         raise ModelError(msg)
+    if rc == BL_ERR_IO:
+        raise IoError(msg)
     if rc == BL_ERR_CAPACITY:
         raise CapacityError(msg, total)
     raise RuntimeError(f"blinkline_b200: {msg}")
@@ -219,6 +240,24 @@ class Context:
                                     int(model.get("window_cells", 10)), int(model.get("cell_px", 8)),
                                     int(model.get("scale_num", 5)), int(model.get("scale_den", 6)),
                                     float(model.get("min_face_ratio", 0.2))))
+
+    def load_detector(self, path):
+        """Parse a "hog-v1" model file (load_detector_model) and upload it."""
+        self.upload_detector(read_detector_json(path))
+
+    def load_ert(self, path):
+        """Parse an "ert-v1" model file (load_ert_model) and upload it without a host copy
+        through Python."""
+        h = _vp()
+        dims = [C.c_int() for _ in range(4)]
+        sh = C.c_double()
+        _err(lib.bl_ert_file_open(os.fsencode(path), C.byref(h), *[C.byref(d) for d in dims], C.byref(sh)))
+        try:
+            _err(lib.bl_ert_file_upload(h, self._h))
+        finally:
+            lib.bl_ert_file_close(h)
+        self.ert_L = dims[0].value
+        self.ert_TK = dims[1].value * dims[2].value
 
     def upload_ert(self, ert):
         m = _np(ert["mean_xy"], np.float64)
@@ -537,3 +576,76 @@ def predict_landmarks(img, box, ert, want_leaves=False):
     ctx = _with_ert(ert)
     r = ctx.landmarks(img, [0], [list(box)], want_leaves=want_leaves)
     return (r[0][0], r[1][0]) if want_leaves else r[0]
+
+
+# ------------------------------------------------------------------ data formats
+def read_pgm(path):
+    """load_pgm (image.hpp:25) as an (h, w) uint8 array (PGM samples are integers <= 255)."""
+    w, h = C.c_int(), C.c_int()
+    p = os.fsencode(path)
+    _err(lib.bl_read_pgm(p, C.byref(w), C.byref(h), None, 0))
+    out = np.empty((h.value, w.value), np.uint8)
+    _err(lib.bl_read_pgm(p, C.byref(w), C.byref(h), out.ctypes.data, out.size))
+    return out
+
+
+def write_pgm(path, img):
+    """save_pgm (image.hpp:28): binary P5, values clamped to [0, 255] and rounded."""
+    a = _np(img, np.float64)
+    _err(lib.bl_write_pgm(os.fsencode(path), a.ctypes.data, a.shape[1], a.shape[0]))
+
+
+def read_detector_json(path):
+    """load_detector_model (detector.hpp:100) -> the dict Context.upload_detector takes."""
+    p = os.fsencode(path)
+    thr, mfr = C.c_double(), C.c_double()
+    wc, cp, sn, sd = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    _err(lib.bl_read_detector_json(p, None, None, C.byref(thr), C.byref(wc), C.byref(cp), C.byref(sn), C.byref(sd),
+                                   C.byref(mfr)))
+    w = np.empty((5, wc.value * wc.value * 31), np.float64)
+    b = np.empty(5, np.float64)
+    _err(lib.bl_read_detector_json(p, w.ctypes.data, b.ctypes.data, C.byref(thr), C.byref(wc), C.byref(cp),
+                                   C.byref(sn), C.byref(sd), C.byref(mfr)))
+    return {"weights": w, "biases": b, "threshold": thr.value, "window_cells": wc.value, "cell_px": cp.value,
+            "scale_num": sn.value, "scale_den": sd.value, "min_face_ratio": mfr.value}
+
+
+def write_detector_json(path, model):
+    """save_model(DetectorModel) (detector.hpp:99)."""
+    w = _np(model["weights"], np.float64).reshape(5, -1)
+    b = _np(model["biases"], np.float64).reshape(5)
+    _err(lib.bl_write_detector_json(os.fsencode(path), w.ctypes.data, b.ctypes.data, float(model["threshold"]),
+                                    int(model.get("window_cells", 10)), int(model.get("cell_px", 8)),
+                                    int(model.get("scale_num", 5)), int(model.get("scale_den", 6)),
+                                    float(model.get("min_face_ratio", 0.2))))
+
+
+def read_ert_json(path):
+    """load_ert_model (ert.hpp:129) -> the dict Context.upload_ert takes."""
+    h = _vp()
+    L, T, K, F = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    sh = C.c_double()
+    _err(lib.bl_ert_file_open(os.fsencode(path), C.byref(h), C.byref(L), C.byref(T), C.byref(K), C.byref(F),
+                              C.byref(sh)))
+    try:
+        S, NL = (1 << F.value) - 1, 1 << F.value
+        n = T.value * K.value
+        out = {"L": L.value, "T": T.value, "K": K.value, "F": F.value, "shrinkage": sh.value,
+               "mean_xy": np.empty((L.value, 2), np.float64),
+               "anchors": np.empty((n * S, 2), np.int32), "split_params": np.empty((n * S, 5), np.float64),
+               "leaves": np.empty((n * NL, L.value, 2), np.float64)}
+        _err(lib.bl_ert_file_copy(h, out["mean_xy"].ctypes.data, out["anchors"].ctypes.data,
+                                  out["split_params"].ctypes.data, out["leaves"].ctypes.data))
+        return out
+    finally:
+        lib.bl_ert_file_close(h)
+
+
+def write_ert_json(path, ert):
+    """save_model(ErtModel) (ert.hpp:128)."""
+    m = _np(ert["mean_xy"], np.float64)
+    a = _np(ert["anchors"], np.int32)
+    s = _np(ert["split_params"], np.float64)
+    lv = _np(ert["leaves"], np.float64)
+    _err(lib.bl_write_ert_json(os.fsencode(path), int(ert["L"]), int(ert["T"]), int(ert["K"]), int(ert["F"]),
+                               float(ert["shrinkage"]), m.ctypes.data, a.ctypes.data, s.ctypes.data, lv.ctypes.data))

@@ -27,6 +27,7 @@ void check(int rc) {
   const std::string msg = bl_last_error();
   if (rc == BL_ERR_INVALID) throw std::invalid_argument(msg);
   if (rc == BL_ERR_MODEL) throw model_error(msg);
+  if (rc == BL_ERR_IO) throw io_error(msg);
   throw std::runtime_error("blinkline_b200: " + msg);
 }
 
@@ -617,4 +618,135 @@ std::vector<FrameResult> detect_and_landmark(const std::vector<GrayImage>& frame
 }
 
 }  // namespace gpu
+// ------------------------------------------------------------------ data formats ----
+// PGM and model files through the C-ABI adapters (bl_io.cpp): same formats, messages and
+// exception classes as image.cpp:67-127, detector.cpp:291-351, ert.cpp:340-469.
+GrayImage load_pgm(const std::string& path) {
+  int w = 0, h = 0;
+  check(bl_read_pgm(path.c_str(), &w, &h, nullptr, 0));
+  std::vector<std::uint8_t> px(std::size_t(w) * h);
+  check(bl_read_pgm(path.c_str(), &w, &h, px.data(), px.size()));
+  GrayImage img = make_image(w, h);
+  for (std::size_t i = 0; i < px.size(); ++i) img.pixels[i] = double(px[i]);
+  return img;
+}
+
+void save_pgm(const GrayImage& img, const std::string& path) {
+  check(bl_write_pgm(path.c_str(), img.pixels.data(), img.width, img.height));
+}
+
+void save_model(const DetectorModel& model, const std::string& path) {
+  const std::size_t per = std::size_t(model.window_cells) * model.window_cells * kCellFeatures;
+  std::vector<double> w(per * 5), b(5);
+  for (int r = 0; r < 5; ++r) {
+    if (model.filters[r].weights.size() != per)
+      throw model_error(path + ": filter " + std::to_string(r) + " does not match window_cells");
+    std::copy(model.filters[r].weights.begin(), model.filters[r].weights.end(), w.begin() + r * per);
+    b[r] = model.filters[r].bias;
+  }
+  check(bl_write_detector_json(path.c_str(), w.data(), b.data(), model.detection_threshold, model.window_cells,
+                               model.cell_px, model.scale_num, model.scale_den, model.min_face_ratio));
+}
+
+DetectorModel load_detector_model(const std::string& path) {
+  DetectorModel m;
+  check(bl_read_detector_json(path.c_str(), nullptr, nullptr, &m.detection_threshold, &m.window_cells, &m.cell_px,
+                              &m.scale_num, &m.scale_den, &m.min_face_ratio));
+  const std::size_t per = std::size_t(m.window_cells) * m.window_cells * kCellFeatures;
+  std::vector<double> w(per * 5), b(5);
+  check(bl_read_detector_json(path.c_str(), w.data(), b.data(), &m.detection_threshold, &m.window_cells, &m.cell_px,
+                              &m.scale_num, &m.scale_den, &m.min_face_ratio));
+  for (int r = 0; r < 5; ++r) {
+    m.filters[r].weights.assign(w.begin() + r * per, w.begin() + (r + 1) * per);
+    m.filters[r].bias = b[r];
+  }
+  return m;
+}
+
+void save_model(const ErtModel& model, const std::string& path) {
+  const int L = model.landmark_count(), T = model.levels(), K = model.trees_per_level();
+  const int F = (T > 0 && K > 0) ? model.cascade[0][0].depth : 0;
+  const std::size_t S = (std::size_t(1) << F) - 1, NL = std::size_t(1) << F;
+  std::vector<double> mean(2 * std::size_t(L)), sp, lv;
+  std::vector<std::int32_t> an;
+  for (int i = 0; i < L; ++i) {
+    mean[2 * i] = model.mean_shape.points[i].x;
+    mean[2 * i + 1] = model.mean_shape.points[i].y;
+  }
+  for (const auto& level : model.cascade) {
+    if (int(level.size()) != K) throw model_error(path + ": every cascade level must carry K trees");
+    for (const RegressionTree& tree : level) {
+      if (tree.splits.size() != S || tree.leaves.size() != NL)
+        throw model_error(path + ": tree split/leaf counts do not match depth F");
+      for (const SplitNode& n : tree.splits) {
+        an.push_back(n.anchor_a);
+        an.push_back(n.anchor_b);
+        for (double v : {n.offset_a.x, n.offset_a.y, n.offset_b.x, n.offset_b.y, n.threshold}) sp.push_back(v);
+      }
+      for (const auto& leaf : tree.leaves)
+        for (const Point2& p : leaf) {
+          lv.push_back(p.x);
+          lv.push_back(p.y);
+        }
+    }
+  }
+  check(bl_write_ert_json(path.c_str(), L, T, K, F, model.shrinkage, mean.data(), an.data(), sp.data(), lv.data()));
+}
+
+ErtModel load_ert_model(const std::string& path) {
+  bl_ert_file* f = nullptr;
+  int L = 0, T = 0, K = 0, F = 0;
+  ErtModel m;
+  check(bl_ert_file_open(path.c_str(), &f, &L, &T, &K, &F, &m.shrinkage));
+  const std::size_t S = (std::size_t(1) << F) - 1, NL = std::size_t(1) << F, n = std::size_t(T) * K;
+  std::vector<double> mean(2 * std::size_t(L)), sp(n * S * 5), lv(n * NL * L * 2);
+  std::vector<std::int32_t> an(n * S * 2);
+  const int rc = bl_ert_file_copy(f, mean.data(), an.data(), sp.data(), lv.data());
+  bl_ert_file_close(f);
+  check(rc);
+  m.mean_shape.frame = ShapeFrame::normalized;
+  for (int i = 0; i < L; ++i) m.mean_shape.points.push_back({mean[2 * i], mean[2 * i + 1]});
+  for (int t = 0; t < T; ++t) {
+    std::vector<RegressionTree> level;
+    for (int k = 0; k < K; ++k) {
+      const std::size_t tk = std::size_t(t) * K + k;
+      RegressionTree tree;
+      tree.depth = F;
+      for (std::size_t s = 0; s < S; ++s) {
+        const std::size_t i = tk * S + s;
+        SplitNode node;
+        node.anchor_a = an[2 * i];
+        node.anchor_b = an[2 * i + 1];
+        node.offset_a = {sp[5 * i], sp[5 * i + 1]};
+        node.offset_b = {sp[5 * i + 2], sp[5 * i + 3]};
+        node.threshold = sp[5 * i + 4];
+        tree.splits.push_back(node);
+      }
+      for (std::size_t q = 0; q < NL; ++q) {
+        std::vector<Point2> delta(L);
+        const double* d = &lv[((tk * NL + q) * L) * 2];
+        for (int i = 0; i < L; ++i) delta[i] = {d[2 * i], d[2 * i + 1]};
+        tree.leaves.push_back(std::move(delta));
+      }
+      level.push_back(std::move(tree));
+    }
+    m.cascade.push_back(std::move(level));
+  }
+  return m;
+}
+
+EyeIndices eye_indices(int landmark_count) {  // ert.cpp:340-347: the iBUG 300-W 68-point convention
+  if (landmark_count != 68)
+    throw std::invalid_argument("eye_indices: no eye mapping for L=" + std::to_string(landmark_count) +
+                                "; only the 68-landmark convention is built in");
+  return EyeIndices{{36, 37, 38, 39, 40, 41}, {42, 43, 44, 45, 46, 47}};
+}
+
+EyeIndices eye_indices(int landmark_count, const EyeIndices& custom) {  // ert.cpp:349-356
+  for (const auto& eye : {custom.left, custom.right})
+    for (const int i : eye)
+      if (i < 0 || i >= landmark_count) throw std::invalid_argument("eye_indices: custom index out of range");
+  return custom;
+}
+
 }  // namespace blinkline

@@ -7,8 +7,9 @@
 // are built from) recompiles against this header and links libblinkline_gpu.so instead.
 // Every function below is implemented on top of the C-ABI in include/blinkline_b200.h.
 //
-// Out of scope (not declared here): PGM I/O, the trainers, model JSON I/O, blink/eval
-// analysis and the pipeline runtime -- see DESIGN.md §6.
+// Also the data formats either side of the path: PGM frames and
+// the "hog-v1" / "ert-v1" model files, through the C-ABI adapters.  Out of scope (not
+// declared here): the trainers, blink/eval analysis and the pipeline runtime -- DESIGN.md §8.
 #pragma once
 
 #include <array>
@@ -40,6 +41,9 @@ struct GrayImage {
 };
 
 GrayImage make_image(int width, int height, double fill = 0.0);
+// P5/P2 PGM, maxval <= 255 (image.hpp:23-28); malformed files throw io_error with the byte offset.
+GrayImage load_pgm(const std::string& path);
+void save_pgm(const GrayImage& img, const std::string& path);
 GrayImage downscale_bilinear(const GrayImage& img);
 
 struct Pyramid {
@@ -144,6 +148,9 @@ std::vector<Detection> threshold_detections(const SaliencyMap& sal, const Detect
 std::vector<Detection> nms(std::vector<Detection> dets, double iou_threshold = 0.5);
 std::vector<int> eligible_scales(int img_w, int img_h, const DetectorModel& model, int n_levels);
 std::vector<Detection> detect_faces(const GrayImage& img, const DetectorModel& model);
+// JSON model file, format version "hog-v1" (detector.hpp:97-100).
+void save_model(const DetectorModel& model, const std::string& path);
+DetectorModel load_detector_model(const std::string& path);
 
 // --------------------------------------------------------------------- ert (ert.hpp)
 struct Point2 {
@@ -204,6 +211,18 @@ struct PredictStats {
 
 Shape predict_landmarks(const GrayImage& img, const Box& box, const ErtModel& model,
                         PredictStats* stats = nullptr);
+
+struct EyeIndices {
+  std::array<int, 6> left;
+  std::array<int, 6> right;
+};
+// iBUG 300-W convention for 68 landmarks: left eye 36..41, right eye 42..47 (ert.hpp:116-125).
+EyeIndices eye_indices(int landmark_count);
+EyeIndices eye_indices(int landmark_count, const EyeIndices& custom);
+
+// JSON model file, format version "ert-v1" (ert.hpp:127-129).
+void save_model(const ErtModel& model, const std::string& path);
+ErtModel load_ert_model(const std::string& path);
 
 // ------------------------------------------------------------ batch extensions (new)
 namespace gpu {

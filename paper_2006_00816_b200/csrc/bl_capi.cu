@@ -36,6 +36,15 @@ int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
+}  // namespace
+
+namespace blb {
+// The thread-local error message, for the host-only translation units (bl_io.cpp).
+void set_last_error(const char* msg) { g_err = msg; }
+}  // namespace blb
+
+namespace {
+
 #define CK(call)                                                                          \
   do {                                                                                    \
     cudaError_t e_ = (call);                                                              \

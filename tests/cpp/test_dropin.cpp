@@ -8,12 +8,15 @@
 // Exit code = number of failed checks.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
+
+#include <unistd.h>
 
 #include "blinkline_gpu.hpp"
 
@@ -121,6 +124,72 @@ static void host_tests() {
   CHECK(leaf[0].x == 2.0);
   // error types
   CHECK_THROWS_AS(make_image(0, 5), std::invalid_argument);
+
+  // data formats (test_image.cpp:50-119, test_detector.cpp:353-394, test_ert.cpp:406-443)
+  const std::string dir = "/tmp/blinkline_dropin_" + std::to_string(::getpid());
+  std::system(("mkdir -p " + dir).c_str());
+  GrayImage pg = make_image(7, 5);
+  for (std::size_t i = 0; i < pg.pixels.size(); ++i) pg.pixels[i] = double((i * 37) % 256);
+  save_pgm(pg, dir + "/f.pgm");
+  const GrayImage back = load_pgm(dir + "/f.pgm");
+  CHECK(back.width == 7 && back.height == 5 && back.pixels == pg.pixels);
+  CHECK_THROWS_AS(load_pgm(dir + "/missing.pgm"), io_error);
+  {
+    std::ofstream(dir + "/bad.pgm") << "P5\n2 2\n300\n";
+    bool msg_ok = false;
+    try {
+      load_pgm(dir + "/bad.pgm");
+    } catch (const io_error& e) {
+      msg_ok = std::string(e.what()).find("unsupported maxval 300 (limit 255) at byte") != std::string::npos;
+    }
+    CHECK(msg_ok);
+  }
+  DetectorModel dm;
+  std::mt19937_64 rng(11);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  for (auto& f : dm.filters) {
+    for (double& wv : f.weights) wv = u(rng);
+    f.bias = u(rng);
+  }
+  dm.detection_threshold = 0.25;
+  save_model(dm, dir + "/hog.json");
+  const DetectorModel dm2 = load_detector_model(dir + "/hog.json");
+  bool same = dm2.detection_threshold == dm.detection_threshold && dm2.window_cells == 10;
+  for (int r = 0; r < 5; ++r) same = same && dm2.filters[r].weights == dm.filters[r].weights && dm2.filters[r].bias == dm.filters[r].bias;
+  CHECK(same);
+  std::ofstream(dir + "/v2.json") << "{\"version\": \"hog-v2\"}";
+  CHECK_THROWS_AS(load_detector_model(dir + "/v2.json"), model_error);
+  CHECK_THROWS_AS(load_detector_model(dir + "/none.json"), io_error);
+  ErtModel em;
+  em.shrinkage = 0.1;
+  for (int i = 0; i < 4; ++i) em.mean_shape.points.push_back({0.1 * i, 0.2 * i});
+  for (int t = 0; t < 2; ++t) {
+    std::vector<RegressionTree> level;
+    for (int k = 0; k < 3; ++k) {
+      RegressionTree tr;
+      tr.depth = 2;
+      for (int sidx = 0; sidx < 3; ++sidx) tr.splits.push_back(SplitNode{sidx % 4, (sidx + 1) % 4, {u(rng), u(rng)}, {u(rng), u(rng)}, u(rng)});
+      for (int l = 0; l < 4; ++l) tr.leaves.push_back({{u(rng), u(rng)}, {u(rng), u(rng)}, {u(rng), u(rng)}, {u(rng), u(rng)}});
+      level.push_back(tr);
+    }
+    em.cascade.push_back(level);
+  }
+  save_model(em, dir + "/ert.json");
+  const ErtModel em2 = load_ert_model(dir + "/ert.json");
+  bool esame = em2.levels() == 2 && em2.trees_per_level() == 3 && em2.landmark_count() == 4 && em2.shrinkage == 0.1;
+  for (int t = 0; esame && t < 2; ++t)
+    for (int k = 0; k < 3; ++k) {
+      const RegressionTree &a = em.cascade[t][k], &b2 = em2.cascade[t][k];
+      for (int sidx = 0; sidx < 3; ++sidx)
+        esame = esame && a.splits[sidx].anchor_a == b2.splits[sidx].anchor_a &&
+                a.splits[sidx].offset_b.y == b2.splits[sidx].offset_b.y && a.splits[sidx].threshold == b2.splits[sidx].threshold;
+      for (int l = 0; l < 4; ++l)
+        for (int i = 0; i < 4; ++i) esame = esame && a.leaves[l][i].x == b2.leaves[l][i].x && a.leaves[l][i].y == b2.leaves[l][i].y;
+    }
+  CHECK(esame);
+  CHECK(eye_indices(68).left[0] == 36 && eye_indices(68).right[5] == 47);
+  CHECK_THROWS_AS(eye_indices(5), std::invalid_argument);
+  std::system(("rm -rf " + dir).c_str());
 }
 
 // -------------------------------------------------------------------------- GPU ----
