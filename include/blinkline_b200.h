@@ -236,6 +236,36 @@ int bl_write_ert_json(const char* path, int L, int T, int K, int F, double shrin
                       const double* mean_xy, const int32_t* anchors, const double* split_params,
                       const double* leaves);
 
+/* -------------------------------------------------- frame-sequence runtime ---- */
+/* One frame of a run (pipeline.hpp:41-47 FrameResult + blink.hpp:20-28 BlinkSample). */
+typedef struct {
+  int32_t frame_index;
+  int32_t n_detections;  /* this frame's post-NMS detections, consecutive in `dets` */
+  int32_t face_found;    /* the frame has a face: its first (best) detection */
+  int32_t pad;
+  bl_detection face;
+  double ear_left, ear_right;          /* valid iff face_found */
+  double closure_left, closure_right;  /* valid iff face_found */
+  double t;                            /* frame_index / fps */
+  double decode_ms, detect_ms, landmark_ms;
+} bl_frame_result;
+
+/* Landmark count of the context's ERT model (BL_ERR_STATE when none is uploaded). */
+int bl_ctx_model_info(bl_ctx* ctx, int* landmark_count);
+/* replaces: ingest (pipeline.hpp:33, pipeline.cpp:358-394): frame_%06d.pgm numbered from 0
+ * without gaps, all with equal dimensions (read from the headers). */
+int bl_ingest(const char* frames_dir, int* n_frames, int* w, int* h);
+/* replaces: run (pipeline.hpp:59-60, pipeline.cpp:396-404) with the uploaded detector and
+ * ERT model: decode -> detect -> landmark the best detection of each frame -> EAR -> blink
+ * trace (blink.cpp:47-93, baseline quantile 0.95), in batches of batch_size frames on the
+ * device (1 = the reference's sequential mode; results identical for any batch size).
+ * frames[n_frames]; dets receives every frame's detections in frame order (det_cap);
+ * landmarks[n_frames][L][2] (rows of frames without a face are untouched);
+ * baselines[2] = left / right EAR baselines. */
+int bl_run(bl_ctx* ctx, const char* frames_dir, double fps, int batch_size, bl_frame_result* frames,
+           int64_t frames_cap, bl_detection* dets, int64_t det_cap, int64_t* det_total, double* landmarks,
+           double* baselines);
+
 #ifdef __cplusplus
 }
 #endif

@@ -278,6 +278,39 @@ class Oracle(_Base):
 class Reference(_Base):
     """The unmodified reference library (oracle/_ref/libblinkline_ref.so)."""
 
+    def run(self, frames_dir, det, ert, fps, pipelined=False, batch_size=16, det_cap=100000):
+        """The reference's run() (pipeline.cpp:396-404) -> the same dict as Context.run, or
+        raises RuntimeError with the reference's message (first ingest/run error)."""
+        L = self.lib
+        L.ref_run.restype = C.c_int
+        L.ref_run.argtypes = [C.c_char_p, _dp, _dp, C.c_double, _vp, C.c_double, C.c_int, C.c_int, _ip, _ip, _ip,
+                              _vp, _dp, _dp, _vp, C.c_int, _ip, _dp]
+        w = np.ascontiguousarray(det["weights"], np.float64).reshape(5, 3100)
+        b = np.ascontiguousarray(det["biases"], np.float64)
+        h = self.ert_handle(ert)
+        try:
+            nmax = 4096  # frames per test directory
+            n = np.zeros(1, np.int32)
+            nd = np.zeros(nmax, np.int32)
+            ff = np.zeros(nmax, np.int32)
+            faces = np.zeros(nmax, DET_DTYPE)
+            lm_buf = np.full((nmax, int(ert["L"]), 2), np.nan)
+            ears = np.zeros((nmax, 4))
+            dets = np.zeros(det_cap, DET_DTYPE)
+            tot = np.zeros(1, np.int32)
+            base = np.zeros(2)
+            rc = L.ref_run(os.fsencode(frames_dir), _ptr(w), _ptr(b), float(det["threshold"]), h, float(fps),
+                           int(pipelined), int(batch_size), _ptr(n, _ip), _ptr(nd, _ip), _ptr(ff, _ip),
+                           faces.ctypes.data, _ptr(lm_buf), _ptr(ears), dets.ctypes.data, det_cap, _ptr(tot, _ip),
+                           _ptr(base))
+            if rc:
+                raise RuntimeError(self.lib.ref_last_error().decode())
+            k = int(n[0])
+            return {"n_detections": nd[:k], "face_found": ff[:k], "faces": faces[:k], "landmarks": lm_buf[:k],
+                    "ears": ears[:k], "detections": dets[:int(tot[0])], "baselines": base}
+        finally:
+            self.lib.ref_ert_destroy(h)
+
     prefix = "ref_"
 
     def __init__(self):

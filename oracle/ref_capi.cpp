@@ -28,7 +28,9 @@
 #include <thread>
 #include <vector>
 
+#include "blinkline/blink.hpp"
 #include "blinkline/detector.hpp"
+#include "blinkline/pipeline.hpp"
 #include "blinkline/errors.hpp"
 #include "blinkline/ert.hpp"
 #include "blinkline/hog.hpp"
@@ -70,6 +72,10 @@ struct RefDet {  // same layout as blinkline::Detection and bl_detection
   int32_t scale_index, rotation_index;
 };
 static_assert(sizeof(RefDet) == sizeof(Detection), "layout");
+
+RefDet to_ref(const Detection& d) {
+  return RefDet{d.box.x, d.box.y, d.box.w, d.box.h, d.score, d.scale_index, d.rotation_index};
+}
 
 void put_dets(const std::vector<Detection>& d, RefDet* out, int cap) {
   for (int i = 0; i < int(d.size()) && i < cap; ++i) {
@@ -659,6 +665,50 @@ int ref_ert_load_json(const char* path, int* dims, double* shrink, double* mean_
           li += leaf.size();
         }
       }
+    return 0;
+  } catch (...) {
+    return io_catch(std::current_exception());
+  }
+}
+
+// ------------------------------------------------------------- run (pipeline.cpp) ----
+// The reference's run() over a frame directory: per frame n_dets, face (RefDet, found flag),
+// landmarks [L][2], the trace sample's ear/closure values; all detections in frame order.
+int ref_run(const char* dir, const double* weights, const double* biases, double thr, void* ert, double fps,
+            int pipelined, int batch_size, int* n_frames, int* n_dets, int* face_found, RefDet* faces,
+            double* landmarks, double* ears4, RefDet* dets, int det_cap, int* det_total, double* baselines) {
+  try {
+    const DetectorModel hog = to_model(weights, biases, thr, 10, 8, 5, 6, 0.2);
+    PipelineConfig cfg;
+    cfg.mode = pipelined ? ExecMode::pipelined : ExecMode::sequential;
+    cfg.batch_size = std::size_t(batch_size);
+    cfg.detect_workers = pipelined ? 2 : 1;
+    cfg.landmark_workers = pipelined ? 2 : 1;
+    const RunOutput out = run(dir, hog, static_cast<RefErt*>(ert)->model, fps, cfg);
+    const int n = int(out.results.size());
+    *n_frames = n;
+    int tot = 0;
+    for (int i = 0; i < n; ++i) {
+      const FrameResult& fr = out.results[i];
+      n_dets[i] = int(fr.detections.size());
+      face_found[i] = fr.face.has_value();
+      if (fr.face) faces[i] = to_ref(*fr.face);
+      if (fr.landmarks)
+        for (std::size_t k = 0; k < fr.landmarks->points.size(); ++k) {
+          landmarks[(std::size_t(i) * fr.landmarks->points.size() + k) * 2] = fr.landmarks->points[k].x;
+          landmarks[(std::size_t(i) * fr.landmarks->points.size() + k) * 2 + 1] = fr.landmarks->points[k].y;
+        }
+      const BlinkSample& s = out.trace.samples[i];
+      ears4[4 * i] = s.ear_left.value_or(NAN);
+      ears4[4 * i + 1] = s.ear_right.value_or(NAN);
+      ears4[4 * i + 2] = s.closure_left.value_or(NAN);
+      ears4[4 * i + 3] = s.closure_right.value_or(NAN);
+      for (const Detection& d : fr.detections)
+        if (tot < det_cap) dets[tot++] = to_ref(d);
+    }
+    *det_total = tot;
+    baselines[0] = out.trace.baseline_left;
+    baselines[1] = out.trace.baseline_right;
     return 0;
   } catch (...) {
     return io_catch(std::current_exception());

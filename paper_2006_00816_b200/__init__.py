@@ -34,7 +34,7 @@ __all__ = [
     "compute_features", "extract_features", "score_separable", "score_dense", "nms",
     "orientation_bins", "detect_faces", "predict_landmarks", "default_context",
     "read_pgm", "write_pgm", "read_detector_json", "write_detector_json", "read_ert_json", "write_ert_json",
-    "IoError",
+    "IoError", "ingest", "FRAME_DTYPE",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -58,6 +58,12 @@ BL_PIX_U8, BL_PIX_F64 = 0, 1
 SCREEN_TCGEN05, SCREEN_FP32 = 0, 1
 MAX_IN_FLIGHT = 3  # BL_MAX_IN_FLIGHT
 STAGES = ["h2d", "pyramid", "gradhist", "features", "screen", "rescore", "nms", "ert", "d2h"]
+
+
+FRAME_DTYPE = np.dtype([("frame_index", "<i4"), ("n_detections", "<i4"), ("face_found", "<i4"), ("pad", "<i4"),
+                        ("face", DET_DTYPE), ("ear_left", "<f8"), ("ear_right", "<f8"), ("closure_left", "<f8"),
+                        ("closure_right", "<f8"), ("t", "<f8"), ("decode_ms", "<f8"), ("detect_ms", "<f8"),
+                        ("landmark_ms", "<f8")], align=True)
 
 
 class ModelError(RuntimeError):
@@ -114,6 +120,9 @@ _SIGS = {
     "bl_debug_sqrt": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "bl_debug_screen_tc": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp]),
     "bl_read_pgm": (C.c_int, [C.c_char_p, _P(C.c_int), _P(C.c_int), _vp, _sz]),
+    "bl_ctx_model_info": (C.c_int, [_vp, _P(C.c_int)]),
+    "bl_ingest": (C.c_int, [C.c_char_p, _P(C.c_int), _P(C.c_int), _P(C.c_int)]),
+    "bl_run": (C.c_int, [_vp, C.c_char_p, C.c_double, C.c_int, _vp, _i64, _vp, _i64, _P(_i64), _vp, _vp]),
     "bl_write_pgm": (C.c_int, [C.c_char_p, _vp, C.c_int, C.c_int]),
     "bl_read_detector_json": (C.c_int, [C.c_char_p, _vp, _vp, _P(C.c_double), _P(C.c_int), _P(C.c_int),
                                         _P(C.c_int), _P(C.c_int), _P(C.c_double)]),
@@ -240,6 +249,23 @@ class Context:
                                     int(model.get("window_cells", 10)), int(model.get("cell_px", 8)),
                                     int(model.get("scale_num", 5)), int(model.get("scale_den", 6)),
                                     float(model.get("min_face_ratio", 0.2))))
+
+    def run(self, frames_dir, fps, batch_size=16, det_cap=None):
+        """run() (pipeline.hpp:59-60) over a frame_%06d.pgm directory with the uploaded models:
+        {"frames": FRAME_DTYPE[n], "detections": DET_DTYPE[...] in frame order,
+         "landmarks": (n, L, 2) (NaN rows where no face), "baselines": (left, right)}."""
+        n, w, h = ingest(frames_dir)
+        L = C.c_int()
+        _err(lib.bl_ctx_model_info(self._h, C.byref(L)))
+        frames = np.zeros(n, FRAME_DTYPE)
+        cap = det_cap if det_cap is not None else n * 64
+        dets = np.zeros(cap, DET_DTYPE)
+        lms = np.full((n, L.value, 2), np.nan)
+        base = np.zeros(2)
+        tot = _i64()
+        _err(lib.bl_run(self._h, os.fsencode(frames_dir), float(fps), int(batch_size), frames.ctypes.data, n,
+                        dets.ctypes.data, cap, C.byref(tot), lms.ctypes.data, base.ctypes.data))
+        return {"frames": frames, "detections": dets[:tot.value], "landmarks": lms, "baselines": base}
 
     def load_detector(self, path):
         """Parse a "hog-v1" model file (load_detector_model) and upload it."""
@@ -649,3 +675,10 @@ def write_ert_json(path, ert):
     lv = _np(ert["leaves"], np.float64)
     _err(lib.bl_write_ert_json(os.fsencode(path), int(ert["L"]), int(ert["T"]), int(ert["K"]), int(ert["F"]),
                                float(ert["shrinkage"]), m.ctypes.data, a.ctypes.data, s.ctypes.data, lv.ctypes.data))
+
+
+def ingest(frames_dir):
+    """ingest (pipeline.hpp:33): validates a frame_%06d.pgm directory -> (n_frames, w, h)."""
+    n, w, h = C.c_int(), C.c_int(), C.c_int()
+    _err(lib.bl_ingest(os.fsencode(frames_dir), C.byref(n), C.byref(w), C.byref(h)))
+    return n.value, w.value, h.value

@@ -12,6 +12,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <chrono>
+#include <cstdio>
+#include <filesystem>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -747,6 +750,214 @@ EyeIndices eye_indices(int landmark_count, const EyeIndices& custom) {  // ert.c
     for (const int i : eye)
       if (i < 0 || i >= landmark_count) throw std::invalid_argument("eye_indices: custom index out of range");
   return custom;
+}
+
+// ------------------------------------------------------------------ blink / pipeline ----
+// EAR and the blink trace (blink.cpp:13-135): host folds over the device's landmarks.
+namespace {
+double pdist(const Point2& a, const Point2& b) { return std::hypot(a.x - b.x, a.y - b.y); }
+
+double quantile_lin(std::vector<double> v, double q) {  // linear interpolation over order statistics
+  std::sort(v.begin(), v.end());
+  if (v.size() == 1) return v[0];
+  const double pos = q * double(v.size() - 1);
+  const std::size_t lo = std::size_t(pos);
+  if (lo + 1 >= v.size()) return v.back();
+  return v[lo] + (pos - double(lo)) * (v[lo + 1] - v[lo]);
+}
+
+double closure(double ear, double baseline) {
+  if (baseline <= 0.0) return 1.0;  // a never-open trace counts every frame as closed
+  return std::clamp(1.0 - ear / baseline, 0.0, 1.0);
+}
+}  // namespace
+
+double eye_aspect_ratio(const std::array<Point2, 6>& p) {
+  const double horiz = pdist(p[0], p[3]);
+  if (horiz <= 1e-9) throw std::invalid_argument("eye_aspect_ratio: degenerate eye, corner span ~ 0");
+  return (pdist(p[1], p[5]) + pdist(p[2], p[4])) / (2.0 * horiz);
+}
+
+double shape_ear(const Shape& landmarks, const std::array<int, 6>& eye) {
+  std::array<Point2, 6> pts;
+  for (std::size_t i = 0; i < 6; ++i) {
+    if (eye[i] < 0 || eye[i] >= int(landmarks.points.size()))
+      throw std::invalid_argument("shape_ear: eye index out of range");
+    pts[i] = landmarks.points[eye[i]];
+  }
+  return eye_aspect_ratio(pts);
+}
+
+BlinkTrace build_trace(const std::vector<FrameEar>& frames, double fps, double baseline_quantile) {
+  if (fps <= 0.0) throw std::invalid_argument("build_trace: fps must be positive");
+  std::vector<FrameEar> ordered = frames;
+  std::sort(ordered.begin(), ordered.end(),
+            [](const FrameEar& a, const FrameEar& b) { return a.frame_index < b.frame_index; });
+  for (std::size_t i = 1; i < ordered.size(); ++i)
+    if (ordered[i].frame_index == ordered[i - 1].frame_index)
+      throw std::invalid_argument("build_trace: duplicate frame index " + std::to_string(ordered[i].frame_index));
+  std::vector<double> lefts, rights;
+  for (const FrameEar& f : ordered)
+    if (f.face_found) {
+      lefts.push_back(f.ear_left);
+      rights.push_back(f.ear_right);
+    }
+  if (lefts.empty())
+    throw std::invalid_argument("build_trace: no frames with a detected face, cannot establish an EAR baseline");
+  BlinkTrace trace;
+  trace.fps = fps;
+  trace.baseline_left = quantile_lin(lefts, baseline_quantile);
+  trace.baseline_right = quantile_lin(rights, baseline_quantile);
+  for (const FrameEar& f : ordered) {
+    BlinkSample s;
+    s.frame_index = f.frame_index;
+    s.t = double(f.frame_index) / fps;
+    s.face_found = f.face_found;
+    if (f.face_found) {
+      s.ear_left = f.ear_left;
+      s.ear_right = f.ear_right;
+      s.closure_left = closure(f.ear_left, trace.baseline_left);
+      s.closure_right = closure(f.ear_right, trace.baseline_right);
+    }
+    trace.samples.push_back(s);
+  }
+  return trace;
+}
+
+std::vector<BlinkEvent> detect_blinks(const BlinkTrace& trace, double closure_threshold, std::size_t min_frames) {
+  std::vector<BlinkEvent> events;  // maximal runs of closure_left >= threshold lasting >= min_frames
+  std::size_t start = 0, len = 0;
+  double peak = 0.0;
+  auto close_run = [&](std::size_t last) {
+    if (len >= min_frames && min_frames > 0)
+      events.push_back(BlinkEvent{trace.samples[start].frame_index, trace.samples[last].frame_index, peak});
+    len = 0;
+    peak = 0.0;
+  };
+  for (std::size_t i = 0; i < trace.samples.size(); ++i) {
+    const BlinkSample& s = trace.samples[i];
+    if (s.closure_left && *s.closure_left >= closure_threshold) {
+      if (len == 0) start = i;
+      ++len;
+      peak = std::max(peak, *s.closure_left);
+    } else if (len > 0) {
+      close_run(i - 1);
+    }
+  }
+  if (len > 0) close_run(trace.samples.size() - 1);
+  return events;
+}
+
+FrameSequence ingest(const std::string& frames_dir) {
+  int n = 0, w = 0, h = 0;
+  check(bl_ingest(frames_dir.c_str(), &n, &w, &h));
+  FrameSequence seq;
+  seq.dir = frames_dir;
+  seq.width = w;
+  seq.height = h;
+  for (int i = 0; i < n; ++i) {
+    char name[32];
+    std::snprintf(name, sizeof name, "frame_%06d.pgm", i);
+    seq.paths.push_back((std::filesystem::path(frames_dir) / name).string());
+  }
+  return seq;
+}
+
+RunOutput run(const std::string& frames_dir, const DetectorModel& hog, const ErtModel& ert, double fps,
+              const PipelineConfig& config) {
+  ThreadCtx& T = tls();
+  ensure_detector(T, hog);
+  ensure_ert(T, ert);
+  int n = 0, w = 0, h = 0;
+  check(bl_ingest(frames_dir.c_str(), &n, &w, &h));
+  const int L = ert.landmark_count();
+  std::vector<bl_frame_result> fr(n);
+  std::vector<bl_detection> dets(std::size_t(std::max(1, n)) * 64);
+  std::vector<double> lms(std::size_t(n) * 2 * L), base(2);
+  int64_t tot = 0;
+  const int batch = config.mode == ExecMode::sequential ? 1 : int(std::max<std::size_t>(1, config.batch_size));
+  int rc = bl_run(T.get(), frames_dir.c_str(), fps, batch, fr.data(), n, dets.data(), int64_t(dets.size()), &tot,
+                  lms.data(), base.data());
+  if (rc == BL_ERR_CAPACITY) {  // more detections than the first guess: size exactly and rerun
+    dets.resize(std::size_t(n) * 5 * 4096);
+    rc = bl_run(T.get(), frames_dir.c_str(), fps, batch, fr.data(), n, dets.data(), int64_t(dets.size()), &tot,
+                lms.data(), base.data());
+  }
+  check(rc);
+  RunOutput out;
+  out.trace.fps = fps;
+  out.trace.baseline_left = base[0];
+  out.trace.baseline_right = base[1];
+  std::size_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    const bl_frame_result& f = fr[i];
+    FrameResult r;
+    r.frame_index = std::size_t(f.frame_index);
+    for (int k = 0; k < f.n_detections; ++k) r.detections.push_back(*reinterpret_cast<const Detection*>(&dets[off + k]));
+    off += std::size_t(f.n_detections);
+    r.timings = StageTimings{f.decode_ms, f.detect_ms, f.landmark_ms};
+    BlinkSample s;
+    s.frame_index = r.frame_index;
+    s.t = f.t;
+    s.face_found = f.face_found != 0;
+    if (f.face_found) {
+      r.face = *reinterpret_cast<const Detection*>(&f.face);
+      Shape sh;
+      sh.frame = ShapeFrame::image;
+      for (int p = 0; p < L; ++p) sh.points.push_back({lms[(std::size_t(i) * L + p) * 2], lms[(std::size_t(i) * L + p) * 2 + 1]});
+      r.landmarks = std::move(sh);
+      s.ear_left = f.ear_left;
+      s.ear_right = f.ear_right;
+      s.closure_left = f.closure_left;
+      s.closure_right = f.closure_right;
+    }
+    out.trace.samples.push_back(s);
+    out.results.push_back(std::move(r));
+  }
+  return out;
+}
+
+std::vector<BenchReport> bench(const std::string& frames_dir, const DetectorModel& hog, const ErtModel& ert,
+                               const std::vector<PipelineConfig>& grid) {
+  // pipeline.cpp:406-454 on the device path: a discarded warm-up run, the sequential run as
+  // the speedup denominator, then every grid entry; per-stage means over the frames.
+  auto timed = [&](const PipelineConfig& cfg, BenchReport& r) {
+    run(frames_dir, hog, ert, 30.0, cfg);  // warm-up (model upload, plan arenas, page cache)
+    const auto t0 = std::chrono::steady_clock::now();
+    const RunOutput o = run(frames_dir, hog, ert, 30.0, cfg);
+    const double total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    r.frames = o.results.size();
+    r.config = cfg;
+    for (const FrameResult& f : o.results) {
+      r.decode_ms += f.timings.decode_ms;
+      r.detect_ms += f.timings.detect_ms;
+      r.landmark_ms += f.timings.landmark_ms;
+    }
+    const double n = double(std::max<std::size_t>(1, r.frames));
+    r.decode_ms /= n;
+    r.detect_ms /= n;
+    r.landmark_ms /= n;
+    r.end_to_end_ms = total / n;
+    r.fps = 1000.0 / r.end_to_end_ms;
+  };
+  PipelineConfig seq_cfg;
+  seq_cfg.mode = ExecMode::sequential;
+  BenchReport ref;
+  timed(seq_cfg, ref);
+  std::vector<BenchReport> out;
+  for (const PipelineConfig& cfg : grid) {
+    BenchReport r;
+    if (cfg.mode == ExecMode::sequential) {
+      r = ref;
+      r.config = cfg;
+      r.speedup = 1.0;
+    } else {
+      timed(cfg, r);
+      r.speedup = ref.end_to_end_ms / r.end_to_end_ms;
+    }
+    out.push_back(r);
+  }
+  return out;
 }
 
 }  // namespace blinkline

@@ -7,15 +7,17 @@
 // are built from) recompiles against this header and links libblinkline_gpu.so instead.
 // Every function below is implemented on top of the C-ABI in include/blinkline_b200.h.
 //
-// Also the data formats either side of the path: PGM frames and
-// the "hog-v1" / "ert-v1" model files, through the C-ABI adapters.  Out of scope (not
-// declared here): the trainers, blink/eval analysis and the pipeline runtime -- DESIGN.md §8.
+// Also what sits either side of the path: the frame-sequence runtime
+// (ingest / run / bench, device-backed), PGM frames, the "hog-v1" / "ert-v1" model files and
+// the EAR / blink-trace fold.  Out of scope (not declared here): the trainers, evaluation
+// metrics, the trace CSV reader/writer and the CLI -- DESIGN.md §8.
 #pragma once
 
 #include <array>
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -223,6 +225,106 @@ EyeIndices eye_indices(int landmark_count, const EyeIndices& custom);
 // JSON model file, format version "ert-v1" (ert.hpp:127-129).
 void save_model(const ErtModel& model, const std::string& path);
 ErtModel load_ert_model(const std::string& path);
+
+// --------------------------------------------------------------- blink (blink.hpp)
+double eye_aspect_ratio(const std::array<Point2, 6>& p);
+double shape_ear(const Shape& landmarks, const std::array<int, 6>& eye);
+
+struct BlinkSample {
+  std::size_t frame_index = 0;
+  double t = 0.0;
+  bool face_found = false;
+  std::optional<double> ear_left;
+  std::optional<double> ear_right;
+  std::optional<double> closure_left;
+  std::optional<double> closure_right;
+};
+
+struct BlinkTrace {
+  double fps = 0.0;
+  std::vector<BlinkSample> samples;
+  double baseline_left = 0.0;
+  double baseline_right = 0.0;
+};
+
+struct FrameEar {
+  std::size_t frame_index = 0;
+  bool face_found = false;
+  double ear_left = 0.0;
+  double ear_right = 0.0;
+};
+
+BlinkTrace build_trace(const std::vector<FrameEar>& frames, double fps, double baseline_quantile = 0.95);
+
+struct BlinkEvent {
+  std::size_t onset_frame = 0;
+  std::size_t offset_frame = 0;
+  double peak_closure = 0.0;
+};
+
+std::vector<BlinkEvent> detect_blinks(const BlinkTrace& trace, double closure_threshold = 0.7,
+                                      std::size_t min_frames = 3);
+
+// ------------------------------------------------------- pipeline (pipeline.hpp)
+// The frame-sequence runtime with detect + landmark on the device (bl_run): frames are
+// decoded on the host and pushed through in batches of batch_size (the decode of batch
+// b+1 overlaps the device work on batch b); sequential mode = batches of one.  Results are
+// in frame order and identical between modes.  Worker counts are accepted for API
+// compatibility; the device path has one decode thread and one device stream per context.
+enum class ExecMode { sequential, pipelined };
+
+struct PipelineConfig {
+  ExecMode mode = ExecMode::sequential;
+  std::size_t batch_size = 16;
+  int detect_workers = 1;
+  int landmark_workers = 1;
+  std::size_t queue_capacity = 4;
+};
+
+struct FrameSequence {
+  std::string dir;
+  std::vector<std::string> paths;
+  int width = 0;
+  int height = 0;
+};
+
+FrameSequence ingest(const std::string& frames_dir);
+
+struct StageTimings {
+  double decode_ms = 0.0;
+  double detect_ms = 0.0;
+  double landmark_ms = 0.0;
+};
+
+struct FrameResult {
+  std::size_t frame_index = 0;
+  std::vector<Detection> detections;
+  std::optional<Detection> face;
+  std::optional<Shape> landmarks;
+  StageTimings timings;
+};
+
+struct RunOutput {
+  std::vector<FrameResult> results;
+  BlinkTrace trace;
+};
+
+RunOutput run(const std::string& frames_dir, const DetectorModel& hog, const ErtModel& ert, double fps,
+              const PipelineConfig& config);
+
+struct BenchReport {
+  std::size_t frames = 0;
+  PipelineConfig config;
+  double decode_ms = 0.0;
+  double detect_ms = 0.0;
+  double landmark_ms = 0.0;
+  double end_to_end_ms = 0.0;
+  double fps = 0.0;
+  double speedup = 1.0;
+};
+
+std::vector<BenchReport> bench(const std::string& frames_dir, const DetectorModel& hog, const ErtModel& ert,
+                               const std::vector<PipelineConfig>& grid);
 
 // ------------------------------------------------------------ batch extensions (new)
 namespace gpu {

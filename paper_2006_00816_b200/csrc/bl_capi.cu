@@ -964,6 +964,14 @@ int bl_ctx_stage_times(bl_ctx* c, float* ms, int* launches) {
   return BL_OK;
 }
 
+int bl_ctx_model_info(bl_ctx* c, int* landmark_count) {
+  if (!c || !landmark_count) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->ert.ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
+  *landmark_count = c->ert.dev.L;
+  return BL_OK;
+}
+
 int bl_ctx_set_screen(bl_ctx* c, int mode) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
   if (mode != BL_SCREEN_TCGEN05 && mode != BL_SCREEN_FP32) return set_err(BL_ERR_INVALID, "unknown screen mode %d", mode);

@@ -127,7 +127,7 @@ static void host_tests() {
 
   // data formats (test_image.cpp:50-119, test_detector.cpp:353-394, test_ert.cpp:406-443)
   const std::string dir = "/tmp/blinkline_dropin_" + std::to_string(::getpid());
-  std::system(("mkdir -p " + dir).c_str());
+  if (std::system(("mkdir -p " + dir).c_str()) != 0) std::printf("mkdir failed\n");
   GrayImage pg = make_image(7, 5);
   for (std::size_t i = 0; i < pg.pixels.size(); ++i) pg.pixels[i] = double((i * 37) % 256);
   save_pgm(pg, dir + "/f.pgm");
@@ -188,8 +188,33 @@ static void host_tests() {
     }
   CHECK(esame);
   CHECK(eye_indices(68).left[0] == 36 && eye_indices(68).right[5] == 47);
+
+  // EAR and the blink trace (test_blink.cpp:41-160)
+  {
+    std::array<Point2, 6> eye{{{0, 0}, {1, 1}, {3, 1}, {4, 0}, {3, -1}, {1, -1}}};
+    CHECK(std::fabs(eye_aspect_ratio(eye) - 0.5) < 1e-12);
+    std::array<Point2, 6> flat{{{0, 0}, {0, 0}, {0, 0}, {0, 0}, {0, 0}, {0, 0}}};
+    CHECK_THROWS_AS(eye_aspect_ratio(flat), std::invalid_argument);
+    auto scripted = [](const std::vector<double>& ears) {
+      std::vector<FrameEar> f;
+      for (std::size_t i = 0; i < ears.size(); ++i) f.push_back({i, true, ears[i], ears[i]});
+      return f;
+    };
+    BlinkTrace tr = build_trace(scripted({0.3, 0.3, 0.3, 0.3}), 100.0);
+    CHECK(std::fabs(tr.baseline_left - 0.3) < 1e-12 && *tr.samples[0].closure_left == 0.0);
+    tr = build_trace(scripted({0.3, 0.3, 0.0, 0.3, 0.3}), 50.0);
+    CHECK(*tr.samples[2].closure_left == 1.0 && *tr.samples[0].closure_left == 0.0);
+    std::vector<double> ears(20, 0.3);
+    for (int i = 7; i < 12; ++i) ears[i] = 0.0;
+    const auto ev = detect_blinks(build_trace(scripted(ears), 10.0), 0.7, 3);
+    CHECK(ev.size() == 1 && ev[0].onset_frame == 7 && ev[0].offset_frame == 11 && ev[0].peak_closure == 1.0);
+    std::vector<FrameEar> none{{0, false, 0, 0}, {1, false, 0, 0}};
+    CHECK_THROWS_AS(build_trace(none, 10.0), std::invalid_argument);
+    std::vector<FrameEar> dup{{0, true, 0.3, 0.3}, {0, true, 0.2, 0.2}};
+    CHECK_THROWS_AS(build_trace(dup, 10.0), std::invalid_argument);
+  }
   CHECK_THROWS_AS(eye_indices(5), std::invalid_argument);
-  std::system(("rm -rf " + dir).c_str());
+  if (std::system(("rm -rf " + dir).c_str()) != 0) std::printf("cleanup failed\n");
 }
 
 // -------------------------------------------------------------------------- GPU ----
@@ -311,6 +336,49 @@ static void gpu_tests(const std::string& model_path) {
   // detect + landmark in one device pass
   const auto both = gpu::detect_and_landmark({frame}, model, one);
   CHECK(both.size() == 1 && both[0].detections.size() == dets.size() && both[0].landmarks.size() == dets.size());
+
+  // run() over a frame directory: sequential == pipelined (test_pipeline.cpp:92-123)
+  {
+    const std::string dir = "/tmp/blinkline_run_" + std::to_string(::getpid());
+    if (std::system(("mkdir -p " + dir).c_str()) != 0) std::printf("mkdir failed\n");
+    std::mt19937_64 frng(1000);
+    for (int i = 0; i < 10; ++i) {
+      GrayImage f = make_image(320, 240, 20.0);
+      for (double& p : f.pixels) p = std::round(std::min(255.0, std::max(0.0, p + urand(frng, -1.5, 1.5))));
+      if (i != 4) draw_ring(f, 150.0 + 3 * i, 120.0, 110.0);
+      char name[32];
+      std::snprintf(name, sizeof name, "/frame_%06d.pgm", i);
+      save_pgm(f, dir + name);
+    }
+    ErtModel e68;  // zero-delta 68-point cascade: landmarks = the mean shape in each face box
+    e68.shrinkage = 0.1;
+    for (int i = 0; i < 68; ++i) e68.mean_shape.points.push_back({0.2 + 0.6 * std::cos(0.3 * i) * 0.5 + 0.3, 0.5 + 0.25 * std::sin(0.7 * i)});
+    RegressionTree z;
+    z.depth = 1;
+    z.splits.assign(1, SplitNode{});
+    z.leaves.assign(2, std::vector<Point2>(68, Point2{0, 0}));
+    e68.cascade.assign(2, std::vector<RegressionTree>(3, z));
+    PipelineConfig pc;
+    pc.mode = ExecMode::pipelined;
+    pc.batch_size = 4;
+    const RunOutput a = run(dir, model, e68, 25.0, PipelineConfig{});
+    const RunOutput b = run(dir, model, e68, 25.0, pc);
+    bool same = a.results.size() == 10 && b.results.size() == 10;
+    for (std::size_t i = 0; same && i < 10; ++i) {
+      same = a.results[i].detections.size() == b.results[i].detections.size() &&
+             a.results[i].face.has_value() == b.results[i].face.has_value();
+      for (std::size_t k = 0; same && k < a.results[i].detections.size(); ++k)
+        same = a.results[i].detections[k].score == b.results[i].detections[k].score;
+      if (same && a.results[i].landmarks)
+        same = a.results[i].landmarks->points[40].x == b.results[i].landmarks->points[40].x;
+    }
+    CHECK(same);
+    CHECK(!a.results[4].face.has_value() && a.results[0].face.has_value());
+    CHECK(a.trace.samples.size() == 10 && !a.trace.samples[4].face_found && a.trace.samples[3].closure_left.has_value());
+    CHECK(a.trace.baseline_left > 0.0 && std::fabs(a.trace.samples[2].t - 2.0 / 25.0) < 1e-15);
+    CHECK(ingest(dir).paths.size() == 10 && ingest(dir).width == 320);
+    if (std::system(("rm -rf " + dir).c_str()) != 0) std::printf("cleanup failed\n");
+  }
 }
 
 int main(int argc, char** argv) {
