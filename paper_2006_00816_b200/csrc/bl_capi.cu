@@ -199,7 +199,14 @@ struct bl_ctx {
   uint64_t launches = 0;
   DetectorState det;
   ErtState ert;
-  Plan plan;
+  // Two detection lanes (plan arenas + compute stream): consecutive in-flight batches
+  // alternate lanes, so batch i+1's pyramid / gradHist overlap batch i's later stages.
+  // Lane 0 runs on the caller's stream (c->user); `plan` / `st` point at the active lane.
+  Plan plans[2];
+  Plan* plan = &plans[0];
+  cudaStream_t lane1 = nullptr;
+  cudaStream_t user = nullptr;
+  cudaEvent_t ev_lane = nullptr;
   // ERT working set
   ErtWork ert_work;  // bl_landmarks' cascade (on the compute stream)
   DevBuf ert_out, ert_leaf, ert_boxes, ert_frames, ert_nfaces, ert_err, ert_input;
@@ -409,7 +416,7 @@ void stage_mark(bl_ctx* c, int stage) {
 // per-frame counts to h_counts (synchronising).
 int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long long pitch,
                long long fstride, int64_t* total_out) {
-  Plan& P = c->plan;
+  Plan& P = *c->plan;
   TRY(build_plan(c, P, n, w, h, pix));
   const Launch L = launch_of(c);
   const DetectorState& D = c->det;
@@ -593,7 +600,7 @@ bool is_pinned_or_device(const void* p) {
 int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, size_t pitch, size_t fstride,
             int landmarks) {
   Slot& S = c->slots[s];
-  Plan& P = c->plan;
+  Plan& P = *c->plan;
   const DetectorState& D = c->det;
   const bool same = P.valid && P.n == n && P.w == w && P.h == h && P.pix == pix &&
                     P.window_cells == D.window_cells && P.cell_px == D.cell_px;
@@ -601,6 +608,8 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
     CK(cudaStreamSynchronize(c->st));
     CK(cudaStreamSynchronize(c->hst));
     CK(cudaStreamSynchronize(c->est));
+    CK(cudaStreamSynchronize(c->lane1));
+    CK(cudaStreamSynchronize(c->user));
     for (Slot& o : c->slots) CK(cudaStreamSynchronize(o.d2h));
   }
   timing_begin(c);
@@ -875,7 +884,9 @@ int bl_ctx_create(int device, bl_ctx** out) {
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&c->est, cudaStreamNonBlocking, lo));
   }
-  c->st = c->own;
+  c->st = c->user = c->own;
+  CK(cudaStreamCreateWithFlags(&c->lane1, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_lane, cudaEventDisableTiming));
   for (Slot& S : c->slots) {
     CK(cudaStreamCreateWithFlags(&S.d2h, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&S.ev_h2d, cudaEventDisableTiming));
@@ -906,6 +917,8 @@ void bl_ctx_destroy(bl_ctx* c) {
   cudaStreamSynchronize(c->st);
   if (c->hst) cudaStreamSynchronize(c->hst);
   if (c->est) cudaStreamSynchronize(c->est);
+  if (c->lane1) cudaStreamSynchronize(c->lane1);
+  if (c->ev_lane) cudaEventDestroy(c->ev_lane);
   if (c->h_counts) cudaFreeHost(c->h_counts);
   for (Slot& S : c->slots) {
     if (S.h_meta) cudaFreeHost(S.h_meta);
@@ -917,7 +930,7 @@ void bl_ctx_destroy(bl_ctx* c) {
       cudaStreamDestroy(S.d2h);
     }
   }
-  cudaStream_t hst = c->hst, est = c->est;
+  cudaStream_t hst = c->hst, est = c->est, lane1 = c->lane1;
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t own = c->own;
@@ -925,12 +938,13 @@ void bl_ctx_destroy(bl_ctx* c) {
   if (own) cudaStreamDestroy(own);
   if (hst) cudaStreamDestroy(hst);
   if (est) cudaStreamDestroy(est);
+  if (lane1) cudaStreamDestroy(lane1);
 }
 
 int bl_ctx_set_stream(bl_ctx* c, void* stream) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
   std::lock_guard<std::mutex> lk(c->mu);
-  c->st = stream ? (cudaStream_t)stream : c->own;
+  c->st = c->user = stream ? (cudaStream_t)stream : c->own;
   return BL_OK;
 }
 
@@ -938,6 +952,7 @@ int bl_ctx_synchronize(bl_ctx* c) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
   TRY(use_device(c));
   CK(cudaStreamSynchronize(c->st));
+  CK(cudaStreamSynchronize(c->lane1));
   CK(cudaStreamSynchronize(c->est));
   CK(cudaStreamSynchronize(c->hst));
   return BL_OK;
@@ -1058,7 +1073,8 @@ int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, d
   CK(cudaMemcpy(D.w32.p, w32.data(), sizeof(float) * w32.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(D.bias64.p, biases, sizeof(double) * kFilters, cudaMemcpyDefault));
   CK(cudaMemcpy(D.cut32.p, D.cut, sizeof(float) * kFilters, cudaMemcpyHostToDevice));
-  c->plan.valid = false;
+  c->plans[0].valid = false;
+  c->plans[1].valid = false;
   D.ready = true;
   return BL_OK;
 }
@@ -1169,7 +1185,17 @@ int bl_submit(bl_ctx* c, const void* frames, int pixel_type, int n, int w, int h
   const int s = (int)(t % BL_MAX_IN_FLIGHT);
   if (c->slots[s].busy)
     return set_err(BL_ERR_STATE, "%d batches in flight: collect one before submitting", BL_MAX_IN_FLIGHT);
-  TRY(enqueue(c, s, frames, pixel_type, n, w, h, pitch, frame_stride, with_landmarks != 0));
+  const int lane = c->timing ? 0 : (int)(t & 1);
+  if (lane == 1) {  // after whatever the caller queued on its stream (e.g. device-resident inputs)
+    CK(cudaEventRecord(c->ev_lane, c->user));
+    CK(cudaStreamWaitEvent(c->lane1, c->ev_lane, 0));
+  }
+  c->plan = &c->plans[lane];
+  c->st = lane ? c->lane1 : c->user;
+  const int rc = enqueue(c, s, frames, pixel_type, n, w, h, pitch, frame_stride, with_landmarks != 0);
+  c->plan = &c->plans[0];
+  c->st = c->user;
+  TRY(rc);
   c->slots[s].ticket = t;
   c->next_ticket = t + 1;
   *ticket = t;
