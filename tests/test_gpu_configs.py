@@ -1,0 +1,88 @@
+"""The BASELINE.json configurations as parity cases (the bench line is C1's 640x480 workload).
+
+Each config runs at its full batch on the device; the CPU oracle checks a seeded subset of
+frames / boxes exactly (it needs seconds per 1080p frame and ~5-10 ms per 15x500x4 face),
+and size-independent properties cover the rest: a frame's result does not depend on the batch
+it rides in (batch invariance), a box's landmarks do not depend on the other boxes (order
+invariance), and repeated runs are bit-identical (determinism).
+
+  C2  320x240 eyeblink stream, batch 16
+  C3  1280x720, batch 64, full pyramid
+  C4  landmark-only: 10k face boxes, 15-cascade x 500-tree depth-4 random-init ERT
+  C5  1920x1080, batch 256 per GPU (here 32 + 8 checked)"""
+
+import numpy as np
+import pytest
+
+from pyoracle import random_ert, ring_frames_np
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_frames(ctx, oracle, model, ert, frames, idx):
+    dets, lms = ctx.detect_landmarks(frames)
+    faces = 0
+    for i in idx:
+        img = frames[i].astype(np.float64)
+        want = oracle.detect_faces(img, model)
+        assert np.array_equal(dets[i], want), i
+        for j, d in enumerate(want[:3]):
+            xy, _, _ = oracle.predict_landmarks(img, (d["x"], d["y"], d["w"], d["h"]), ert)
+            assert np.max(np.abs(lms[i][j] - xy)) <= 1e-9
+            faces += 1
+    return dets, lms, faces
+
+
+def test_c2_qvga_stream_batch16(ctx, oracle, pattern_model):
+    frames = ring_frames_np(16, 320, 240, seed=202)
+    ert = random_ert(T=4, K=100, F=4, seed=21)
+    ctx.upload_detector(pattern_model)
+    ctx.upload_ert(ert)
+    _, _, faces = _check_frames(ctx, oracle, pattern_model, ert, frames, range(16))
+    assert faces >= 12
+
+
+def test_c3_720p_batch64(ctx, oracle, pattern_model):
+    frames = ring_frames_np(64, 1280, 720, seed=303)
+    ert = random_ert(T=3, K=60, F=4, seed=31)
+    ctx.upload_detector(pattern_model)
+    ctx.upload_ert(ert)
+    dets, lms, faces = _check_frames(ctx, oracle, pattern_model, ert, frames, [0, 37, 63])
+    assert faces > 0
+    # batch invariance: frames 8..11 alone give the same results as inside the 64-frame batch
+    d4, l4 = ctx.detect_landmarks(frames[8:12])
+    for k in range(4):
+        assert np.array_equal(d4[k], dets[8 + k]) and np.array_equal(l4[k], lms[8 + k])
+
+
+def test_c4_ert_only_10k_boxes(ctx, oracle):
+    ert = random_ert(L=68, T=15, K=500, F=4, seed=2020)
+    img = np.floor(np.random.default_rng(404).uniform(0, 256, (480, 640)))
+    r = np.random.default_rng(405)
+    n = 10000
+    side = r.integers(120, 280, n)
+    boxes = np.stack([r.integers(0, 640 - side + 1), r.integers(0, 480 - side + 1), side, side], 1).astype(np.int32)
+    ctx.upload_ert(ert)
+    u8 = img.astype(np.uint8)
+    xy, leaves = ctx.landmarks(u8, np.zeros(n, np.int32), boxes, want_leaves=True)
+    assert xy.shape == (n, 68, 2) and leaves.shape == (n, 15 * 500)
+    for i in r.choice(n, 40, replace=False):  # exact leaf indices, landmarks to 1e-9
+        wxy, wl, _ = oracle.predict_landmarks(img, tuple(boxes[i]), ert)
+        assert np.array_equal(leaves[i], wl), i
+        assert np.max(np.abs(xy[i] - wxy)) <= 1e-9
+    # order invariance + determinism on all 10k
+    perm = r.permutation(n)
+    xy2 = ctx.landmarks(u8, np.zeros(n, np.int32), boxes[perm])
+    assert np.array_equal(xy2, xy[perm])
+
+
+def test_c5_1080p_batch(ctx, oracle, pattern_model):
+    frames = ring_frames_np(32, 1920, 1080, seed=505)
+    ert = random_ert(T=2, K=40, F=4, seed=51)
+    ctx.upload_detector(pattern_model)
+    ctx.upload_ert(ert)
+    dets, lms, faces = _check_frames(ctx, oracle, pattern_model, ert, frames, [5, 30])
+    assert faces > 0
+    again = ctx.detect_landmarks(frames)
+    for k in range(32):
+        assert np.array_equal(again[0][k], dets[k]) and np.array_equal(again[1][k], lms[k])
