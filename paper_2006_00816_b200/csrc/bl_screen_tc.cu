@@ -39,8 +39,14 @@ constexpr int kTcN = 64;              // 10 dx x 5 filters = 50 columns, padded
 constexpr int kTcNM = 2;              // m-tiles per work unit
 constexpr int kTcNA = 248;            // cells staged per plane: kTcV * (kTcNM - 1) + kTcM, rounded to 8
 constexpr int kTcPlanes = 8;          // 32 features / 4 per 16-B chunk
-constexpr int kTcStages = 3;
-constexpr int kTcABytes = kTcPlanes * kTcNA * 16;           // 31,744 per stage
+#ifndef BL_TC_J
+#define BL_TC_J 2
+#endif
+constexpr int kTcJ = BL_TC_J;        // window rows per stage: their cell ranges overlap by cw
+constexpr int kTcCwMax = 80;          // levels wider than this stage one window row at a time
+constexpr int kTcNAS = kTcNA + (kTcJ - 1) * kTcCwMax;      // cells per plane per stage
+constexpr int kTcStages = kTcJ > 1 ? 2 : 3;
+constexpr int kTcABytes = kTcPlanes * kTcNAS * 16;          // 41,984 per stage (J = 2)
 constexpr int kTcWRowBytes = kTcPlanes * kTcN * 16;         // 8,192 per window row j
 constexpr int kTcWBytes = kWin * kTcWRowBytes;              // 81,920 resident
 constexpr int kTcEpiBytes = 50 * kTcM * 4;                  // 25,600: Q tile for the dx-correlation
@@ -199,14 +205,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_screen_tc(const PlanDesc* __r
         const LevelDesc& D = P->lv[s];
         const long long ncp = D.tc_ncp;
         const float* fbase = feat_tc + D.tc_off + (long long)f * kTcPlanes * ncp * 4;
-        for (int j = 0; j < kWin; ++j) {
+        const int jpl = D.cw <= kTcCwMax ? kTcJ : 1;
+        for (int j0 = 0; j0 < kWin; j0 += jpl) {
+          // window rows j0 .. j0+J-1 read cells [L0 + j0*cw, L0 + (j0+J-1)*cw + NA): one copy
+          const int J = min(jpl, kWin - j0);
+          const int nc = kTcNA + (J - 1) * D.cw;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = sA + stage * kTcABytes;
-          mbar_expect_tx(&full_bar[stage], kTcABytes);
-          const long long c0 = L0 + (long long)j * D.cw;
+          mbar_expect_tx(&full_bar[stage], (uint32_t)(kTcPlanes * nc * 16));
+          const long long c0 = L0 + (long long)j0 * D.cw;
 #pragma unroll 1
           for (int kc = 0; kc < kTcPlanes; ++kc)
-            bulk_g2s(sa + kc * kTcNA * 16, fbase + ((long long)kc * ncp + c0) * 4, kTcNA * 16, &full_bar[stage]);
+            bulk_g2s(sa + kc * kTcNAS * 16, fbase + ((long long)kc * ncp + c0) * 4, (uint32_t)nc * 16,
+                     &full_bar[stage]);
           if (++stage == kTcStages) {
             stage = 0;
             phase ^= 1;
@@ -223,27 +234,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_screen_tc(const PlanDesc* __r
     uint32_t acc_phase = 0;
     const uint32_t sw0 = smem_u32(sW);
     for (long long u = blockIdx.x; u < total; u += gridDim.x) {
+      int us, uf;
+      long long uL0;
+      unit_info(u, us, uf, uL0);
+      const int cw = P->lv[us].cw;
+      const int jpl = cw <= kTcCwMax ? kTcJ : 1;
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d0 = tmem_base + acc * kTcAccCols;
-      for (int j = 0; j < kWin; ++j) {
+      for (int j0 = 0; j0 < kWin; j0 += jpl) {
+        const int J = min(jpl, kWin - j0);
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sa = smem_u32(sA + stage * kTcABytes);
+#pragma unroll 1
+          for (int jj = 0; jj < J; ++jj) {
+            const int j = j0 + jj;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            // B (weights of row j): [kc][64 n][16 B]: K chunk step 1024 B, 8-row group step 128 B
-            const uint64_t db = umma_desc(sw0 + j * kTcWRowBytes + (2 * kk) * (kTcN * 16), kTcN * 16, 128);
+            for (int kk = 0; kk < 4; ++kk) {
+              // B (weights of row j): [kc][64 n][16 B]: K chunk step 1024 B, 8-row group step 128 B
+              const uint64_t db = umma_desc(sw0 + j * kTcWRowBytes + (2 * kk) * (kTcN * 16), kTcN * 16, 128);
 #pragma unroll
-            for (int m = 0; m < kTcNM; ++m) {
-              // A (cells): [kc][NA cells][16 B]: K chunk step NA*16 B, 8-row group step 128 B
-              const uint64_t da = umma_desc(sa + (uint32_t)(((2 * kk) * kTcNA + m * kTcV) * 16), kTcNA * 16, 128);
-              mma_tf32(d0 + m * kTcN, da, db, (j | kk) != 0);
+              for (int m = 0; m < kTcNM; ++m) {
+                // A (cells of row j): [kc][NAS cells][16 B], row j starts jj*cw cells into the stage
+                const uint64_t da = umma_desc(sa + (uint32_t)(((2 * kk) * kTcNAS + jj * cw + m * kTcV) * 16),
+                                              kTcNAS * 16, 128);
+                mma_tf32(d0 + m * kTcN, da, db, (j | kk) != 0);
+              }
             }
           }
           mma_commit(&empty_bar[stage]);  // frees the smem stage once these MMAs have read it
-          if (j == kWin - 1) mma_commit(&tfull_bar[acc]);
+          if (j0 + J == kWin) mma_commit(&tfull_bar[acc]);
         }
         __syncwarp();
         if (++stage == kTcStages) {
