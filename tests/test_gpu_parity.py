@@ -84,7 +84,11 @@ def test_orientation_exhaustive_integer_gradients(ctx, oracle):
     r = rng(9)
     ang = r.uniform(0, 2 * np.pi, 200000)
     ang2 = (np.arange(36) * np.pi / 18)[:, None] + r.uniform(-1e-12, 1e-12, (36, 2000))  # on/near every tie
-    mags = r.uniform(1e-6, 400, 200000)
+    # the fast path's threshold margin: angles within 1e-8 .. 1e-4 rad of every bin midpoint
+    ang3 = (np.arange(18) * np.pi / 9 + np.pi / 18)[:, None] + \
+        np.sign(r.uniform(-1, 1, (18, 4000))) * np.exp(r.uniform(np.log(1e-8), np.log(1e-4), (18, 4000)))
+    ang = np.concatenate([ang, ang3.ravel()])
+    mags = r.uniform(1e-6, 400, ang.size)
     ex_gx = np.concatenate([gx, mags * np.cos(ang), 10 * np.cos(ang2.ravel()), r.uniform(-1e-13, 1e-13, 1000)])
     ex_gy = np.concatenate([gy, mags * np.sin(ang), 10 * np.sin(ang2.ravel()), r.uniform(-1e-13, 1e-13, 1000)])
     got = ctx.orientation_bins(ex_gx, ex_gy)
