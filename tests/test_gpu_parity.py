@@ -42,6 +42,19 @@ def test_pyramid_matches_oracle(ctx, oracle, w, h):
     assert np.array_equal(sc_o, sc_g)
 
 
+@pytest.mark.parametrize("w,h,win", [(1000, 121, 80), (97, 301, 80), (2000, 130, 80), (333, 1200, 80), (250, 170, 4),
+                                     (33, 700, 2), (4096, 200, 80)])
+def test_pyramid_odd_shapes(ctx, oracle, w, h, win):
+    """Extreme aspect ratios and deep chains down to 2-pixel levels, f64 input (no
+    integral-pixel shortcut)."""
+    img = rng(w + h).uniform(0, 255, (h, w))
+    lv_o, _ = oracle.build_pyramid(img, win)
+    lv_g, _ = ctx.build_pyramid(img, win)
+    assert len(lv_o) == len(lv_g) > 1
+    for a, b in zip(lv_o, lv_g):
+        assert np.array_equal(a, b)
+
+
 def test_pyramid_640x480_dims(ctx):
     levels, _ = ctx.build_pyramid(np.full((480, 640), 10.0), 80)
     assert [lv.shape[0] for lv in levels] == [480, 400, 333, 277, 230, 191, 159, 132, 110, 91]
