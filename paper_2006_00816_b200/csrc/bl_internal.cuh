@@ -32,7 +32,10 @@ constexpr int kMaxLevels = 32;
 
 // gradHist: a warp owns 31 cells of a cell-row strip over a segment of kGhSegRows cell rows.
 constexpr int kGhCells = 31;
-constexpr int kGhSegRows = 12;
+#ifndef BL_HOG_SEG
+#define BL_HOG_SEG 24
+#endif
+constexpr int kGhSegRows = BL_HOG_SEG;
 
 struct LevelDesc {
   int w, h;              // level pixel dims
