@@ -41,7 +41,7 @@ ERT_T, ERT_K, ERT_F = 15, 500, 4
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=40)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--batch", type=int, default=512, help="frames per GPU per step")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -96,7 +96,7 @@ class ClockSampler:
                     self.rows.append([c.strip() for c in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -134,6 +134,12 @@ def geometry():
     return lw, lh, scored
 
 
+# fp64 operations per level pixel in the fused gradHist: gx, gy (2 sub), s = gx^2 + gy^2
+# (2 mul + add), sqrt_fast (4 mul + 4 fma), then per neighbouring cell m*wx and (m*wx)*wy
+# for two open cell rows plus the two adds (2 x 5)
+GRADHIST_FP64_OPS = 2 + 3 + 8 + 10
+
+
 def algorithmic_bytes_per_frame():
     """Canonical per-frame bytes of each stage."""
     lw, lh, scored = geometry()
@@ -144,6 +150,7 @@ def algorithmic_bytes_per_frame():
     return {
         "pyramid": res,
         "gradhist": px + cells * 19 * 8,                  # level pixels read, bins + energy written
+        "gradhist_px": sum(lw[k] * lh[k] for k in scored),  # level pixels (fp64 ops: GRADHIST_FP64_OPS each)
         "features": cells * (19 * 8 + 31 * 8 + 32 * 4),  # bins+energy read, fp64 + tf32 planes written
         "screen": cells * 32 * 4,                         # tf32 feature planes read once
         "anchors": anchors,
@@ -274,6 +281,19 @@ def run_ours(args):
         if k in traffic:
             e["dram_GB_ncu"] = round(traffic[k] * B / 1e9, 3)
         per_stage[k] = e
+    # secondary bounds (profiles/peaks_b200.json, measured on the box by tools/peaks.cu):
+    # gradHist against the fp64 pipe, the ERT cascade against L2 read bandwidth
+    try:
+        sec = json.load(open(os.path.join(ROOT, "profiles", "peaks_b200.json")))
+        if kern_ms["gradhist"] > 0:
+            ops = GRADHIST_FP64_OPS * alg["gradhist_px"] * B / (kern_ms["gradhist"] / 1000.0) / 1e12
+            per_stage["gradhist"].update({"fp64_Tops": round(ops, 2),
+                                          "frac_fp64": round(ops / sec["fp64_add_tflops"], 3)})
+        if kern_ms["ert"] > 0:
+            l2 = ert_bytes / (kern_ms["ert"] / 1000.0) / 1e9
+            per_stage["ert"].update({"frac_l2": round(l2 / sec["l2_read_gbs"], 3)})
+    except Exception:
+        pass
     if kern_ms["screen"] > 0:  # the tcgen05 screen: useful FLOPs (dense 10x10x31 x 5 filters)
         tfs = 2 * 5 * 3100 * alg["anchors"] * B / (kern_ms["screen"] / 1000.0) / 1e12
         per_stage["screen"].update({"TFLOP/s": round(tfs, 1), "frac_tf32": round(tfs / tf32_peak, 3)})
