@@ -227,6 +227,12 @@ void launch_ert_level(const Launch& L, const ErtDev& M, int t, const void* frame
 //   traverse thread per (face, tree): level-order descent, leaf index -> smem;
 //   accum    thread per (face, landmark pair): the K selected leaf rows in tree order.
 // Current shapes, transforms and the level's leaf indices live in shared memory.
+struct TravItem {  // one (face, tree) traversal in flight
+  const void* fr;
+  double2 ab;
+  int X, Y, W, H, k, fi, node;
+};
+
 #ifndef BL_ERT_FACES
 #define BL_ERT_FACES 4
 #endif
@@ -262,30 +268,53 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
       stf[warp] = make_double2(A, B);
     }
     __syncthreads();
-    // (2) traversals
+    // (2) traversals: two (face, tree) items per thread walk their trees in lock-step (all
+    // trees have depth F), so each level's record and pixel loads of both are in flight together
     const SplitRec* lvl = M.split + (long long)t * S * K;
-    for (int e = tid; e < nf * K; e += blockDim.x) {
-      const int fi = e / K, k = e - fi * K;
-      const int face = f0 + fi;
-      const double2 ab = stf[fi];
-      const int* bx = boxes + (long long)face * box_stride;
-      const int X = bx[0], Y = bx[1], W = bx[2], H = bx[3];
-      const void* fr = (const char*)frames + (long long)face_frame[face] * fstride * (U8 ? 1 : 8);
-      const double* cur = sc + fi * L2;
-      int node = 0;
-      while (node < S) {
-        const SplitRec* r = lvl + (long long)node * K + k;
-        const double2 oa = __ldg(reinterpret_cast<const double2*>(r));
-        const double2 ob = __ldg(reinterpret_cast<const double2*>(r) + 1);
-        const int4 tail = __ldg(reinterpret_cast<const int4*>(r) + 2);
-        const double thr = __hiloint2double(tail.y, tail.x);
-        const int an_a = (short)(tail.z & 0xffff), an_b = (short)(tail.z >> 16);
-        const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, cur, ab.x, ab.y, an_a, oa.x, oa.y);
-        const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, cur, ab.x, ab.y, an_b, ob.x, ob.y);
-        node = dsub(ia, ib) > thr ? 2 * node + 1 : 2 * node + 2;  // ert.cpp:87-97
+    const int items = nf * K;
+    for (int e0 = tid; e0 < items; e0 += 2 * blockDim.x) {
+      const int e1 = min(e0 + (int)blockDim.x, items - 1);  // a duplicate of e0's last item when odd
+      TravItem it[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int e = q == 0 ? e0 : e1;
+        const int fi = e / K;
+        it[q].k = e - fi * K;
+        it[q].fi = fi;
+        const int face = f0 + fi;
+        it[q].ab = stf[fi];
+        const int* bx = boxes + (long long)face * box_stride;
+        it[q].X = bx[0];
+        it[q].Y = bx[1];
+        it[q].W = bx[2];
+        it[q].H = bx[3];
+        it[q].fr = (const char*)frames + (long long)face_frame[face] * fstride * (U8 ? 1 : 8);
+        it[q].node = 0;
       }
-      sli[fi * K + k] = (uint8_t)(node - S);
-      if (leaf_out) leaf_out[(long long)face * leaf_out_stride + (long long)t * K + k] = (uint8_t)(node - S);
+      for (int d = 0; d < M.F; ++d) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const SplitRec* r = lvl + (long long)it[q].node * K + it[q].k;
+          const double2 oa = __ldg(reinterpret_cast<const double2*>(r));
+          const double2 ob = __ldg(reinterpret_cast<const double2*>(r) + 1);
+          const int4 tail = __ldg(reinterpret_cast<const int4*>(r) + 2);
+          const double thr = __hiloint2double(tail.y, tail.x);
+          const int an_a = (short)(tail.z & 0xffff), an_b = (short)(tail.z >> 16);
+          const double* cur = sc + it[q].fi * L2;
+          const double ia = sample_px<U8>(it[q].fr, w, h, pitch, it[q].X, it[q].Y, it[q].W, it[q].H, cur,
+                                          it[q].ab.x, it[q].ab.y, an_a, oa.x, oa.y);
+          const double ib = sample_px<U8>(it[q].fr, w, h, pitch, it[q].X, it[q].Y, it[q].W, it[q].H, cur,
+                                          it[q].ab.x, it[q].ab.y, an_b, ob.x, ob.y);
+          it[q].node = dsub(ia, ib) > thr ? 2 * it[q].node + 1 : 2 * it[q].node + 2;  // ert.cpp:87-97
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int leaf = it[q].node - S;
+        sli[it[q].fi * K + it[q].k] = (uint8_t)leaf;
+        if (leaf_out)
+          leaf_out[(long long)(f0 + it[q].fi) * leaf_out_stride + (long long)t * K + it[q].k] = (uint8_t)leaf;
+      }
     }
     __syncthreads();
     // (3) leaf sums in tree order, cur += shrinkage * delta (ert.cpp:118-126)
