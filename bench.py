@@ -2,7 +2,7 @@
 """bench.py -- frames/sec of detect + 68 landmarks @640x480 on B200 (BASELINE.json metric).
 
 Workload (one step, per GPU): B synthetic 640x480 eyeblink-camera frames (u8, seeded ring
-targets) -> pyramid -> gradHist -> features -> tcgen05 tf32 screen -> exact fp64 re-score ->
+targets) -> pyramid -> gradHist -> features -> tcgen05 fp16 screen -> exact fp64 re-score ->
 threshold -> NMS -> ERT 15 x 500 x depth-4 random-init 68-landmark cascade on every kept
 detection.  Models: the reference's own ring-pattern detector (tests/golden/
 pattern_detector.npz, exported from the reference's pattern_detector()) and a seeded
@@ -151,8 +151,8 @@ def algorithmic_bytes_per_frame():
         "pyramid": res,
         "gradhist": px + cells * 19 * 8,                  # level pixels read, bins + energy written
         "gradhist_px": sum(lw[k] * lh[k] for k in scored),  # level pixels (fp64 ops: GRADHIST_FP64_OPS each)
-        "features": cells * (19 * 8 + 31 * 8 + 32 * 4),  # bins+energy read, fp64 + tf32 planes written
-        "screen": cells * 32 * 4,                         # tf32 feature planes read once
+        "features": cells * (19 * 8 + 31 * 8 + 32 * 2),  # bins+energy read, fp64 + fp16 planes written
+        "screen": cells * 32 * 2,                         # fp16 feature planes read once
         "anchors": anchors,
         "cells": cells,
     }
@@ -261,7 +261,7 @@ def run_ours(args):
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    tf32_peak = float(peaks.get("bf16_tflops", 1590.0)) / 2.0  # dense tf32 = half the bf16 rate
+    f16_peak = float(peaks.get("bf16_tflops", 1590.0))  # dense fp16 = the bf16 rate
     traffic = {}
     try:  # ncu dram__bytes_read + write per frame of each stage's kernels (profiles/traffic.json)
         traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bytes_per_frame"]
@@ -296,7 +296,7 @@ def run_ours(args):
         pass
     if kern_ms["screen"] > 0:  # the tcgen05 screen: useful FLOPs (dense 10x10x31 x 5 filters)
         tfs = 2 * 5 * 3100 * alg["anchors"] * B / (kern_ms["screen"] / 1000.0) / 1e12
-        per_stage["screen"].update({"TFLOP/s": round(tfs, 1), "frac_tf32": round(tfs / tf32_peak, 3)})
+        per_stage["screen"].update({"TFLOP/s": round(tfs, 1), "frac_f16": round(tfs / f16_peak, 3)})
     ach = bytes_stage.get(dom, 0) / (kern_ms[dom] / 1000.0) / 1e9
     roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(ach / hbm_peak, 3),

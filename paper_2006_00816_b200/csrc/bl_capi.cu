@@ -114,14 +114,23 @@ int round_half_up_host(double v) { return int(std::floor(v + 0.5)); }  // detect
 
 constexpr int kLevelMargin = 8;  // readable doubles either side of every arena level row
 
-// Round a float to the nearest tf32 value (ties away from zero, like cvt.rna.tf32.f32).
-float tf32_round_host(float x) {
-  uint32_t b;
-  std::memcpy(&b, &x, 4);
-  if ((b & 0x7f800000u) != 0x7f800000u) b = (b + 0x1000u) & ~0x1fffu;
-  float r;
-  std::memcpy(&r, &b, 4);
-  return r;
+// Round a double to the nearest fp16 (ties to even, like cvt.rn.f16.f64); |x| < 65520.
+uint16_t half_rn_host(double x) {
+  const uint16_t sign = std::signbit(x) ? 0x8000 : 0;
+  const double a = std::fabs(x);
+  if (a == 0.0) return sign;
+  int e = 0;
+  std::frexp(a, &e);  // a = m 2^e, m in [0.5, 1): binade exponent e - 1
+  if (e - 1 < -14) {  // subnormal: quantum 2^-24
+    const double q = std::nearbyint(std::ldexp(a, 24));
+    return (uint16_t)(sign | (uint16_t)q);  // q = 1024 encodes the smallest normal
+  }
+  double q = std::nearbyint(std::ldexp(a, 11 - e));  // 11 significant bits, in [1024, 2048]
+  if (q == 2048.0) {
+    q = 1024.0;
+    ++e;
+  }
+  return (uint16_t)(sign | (uint16_t)((e - 1 + 15) << 10) | (uint16_t)((int)q - 1024));
 }
 
 struct DetectorState {
@@ -131,7 +140,7 @@ struct DetectorState {
   double min_face_ratio = 0.2;
   double bias[kFilters] = {0};
   float cut[kFilters] = {0};
-  float cut_tc[kFilters] = {0};
+  float cut_tc[2 * kFilters] = {0};  // [0, 5): cut in the screen's scaled domain, [5, 10): 2^-scale
   double delta_tc[kFilters] = {0};
   DevBuf w64, w32, bias64, cut32, w_tc, cuttc;
 };
@@ -1038,33 +1047,49 @@ int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, d
     if ((double)cf > cutd) cf = std::nextafterf(cf, -INFINITY);
     D.cut[r] = cf;
   }
-  // tcgen05 screen: tf32 (round to nearest) weights [j][kc][64 n = dx * 5 + r][4], and the cut
-  // delta_tc >= |tf32 MMA sum - exact sum|: operands rounded to tf32 (each <= 2^-11 relative,
-  // product <= 2^-10 + 2^-22), fp32 feature rounding 2^-24, fp32 accumulation over 400
-  // MMAs of K = 8 (<= 1024 u even with truncating hardware adds), features <= 0.8486.
-  std::vector<float> wtc(tc_weight_floats(), 0.f);
+  // tcgen05 screen: fp16 weights [j][kc][64 n = dx * 5 + r][8], filter r scaled by 2^ws[r] so
+  // its largest |w| lies in [2^14, 2^15) (exact; fp16 max 65504), features scaled by
+  // 2^kTcFeatExp in k_features.  The screen compares the scaled sum against the scaled cut.
+  // delta_tc >= |fp16 MMA sum - exact sum| in unscaled units: operands rounded to fp16 (each
+  // <= 2^-11 relative when normal, product <= 2^-10 + 2^-22; values in the fp16 subnormal
+  // range carry an absolute error <= 2^-25 of their scaled unit instead: 2^-25-kTcFeatExp per
+  // feature, 2^-25-ws per weight), fp32 accumulation over 200 MMAs of K = 16 (<= 1024 u even
+  // with truncating hardware adds), features <= 0.8486.
+  int ws[kFilters];
+  for (int r = 0; r < kFilters; ++r) {
+    double mx = 0;
+    for (int k = 0; k < kFilterW; ++k) mx = std::max(mx, std::fabs(weights[(size_t)r * kFilterW + k]));
+    int e = 0;
+    if (mx > 0) std::frexp(mx, &e);       // mx in [2^(e-1), 2^e)
+    ws[r] = mx > 0 ? 15 - e : 0;          // mx * 2^ws in [2^14, 2^15)
+    ws[r] = std::max(-100, std::min(100, ws[r]));
+  }
+  std::vector<uint16_t> wtc(tc_weight_floats() * 2, 0);
   for (int j = 0; j < kWin; ++j)
     for (int dx = 0; dx < kWin; ++dx)
       for (int f = 0; f < kFeat; ++f)
         for (int r = 0; r < kFilters; ++r)
-          wtc[(((size_t)j * 8 + f / 4) * 64 + dx * kFilters + r) * 4 + f % 4] =
-              tf32_round_host((float)weights[(size_t)r * kFilterW + j * kRowW + dx * kFeat + f]);
+          wtc[(((size_t)j * kTcPlanesF16 + f / 8) * 64 + dx * kFilters + r) * 8 + f % 8] =
+              half_rn_host(std::ldexp(weights[(size_t)r * kFilterW + j * kRowW + dx * kFeat + f], ws[r]));
   for (int r = 0; r < kFilters; ++r) {
     double l1 = 0;
     for (int k = 0; k < kFilterW; ++k) l1 += std::fabs(weights[(size_t)r * kFilterW + k]);
     const double rel = std::ldexp(1.0, -10) + std::ldexp(1.0, -22) + std::ldexp(1.0, -24) + 1024.0 * u;
-    const double delta = 1.1 * rel * 0.8486 * l1 + std::ldexp(1.0, -20) * (std::fabs(threshold) + std::fabs(biases[r])) + 1e-9;
+    const double sub = l1 * std::ldexp(1.0, -25 - kTcFeatExp) + 0.85 * kFilterW * std::ldexp(1.0, -25 - ws[r]);
+    const double delta = 1.1 * (rel * 0.8486 * l1 + sub) + std::ldexp(1.0, -20) * (std::fabs(threshold) + std::fabs(biases[r])) + 1e-9;
     D.delta_tc[r] = delta;
     const double cutd = threshold - biases[r] - delta;
-    float cf = (float)cutd;
+    const int sc = ws[r] + kTcFeatExp;
+    float cf = (float)std::ldexp(cutd, sc);  // cut in the scaled domain (power-of-two scaling)
     if (std::isnan(cutd)) cf = -INFINITY;
-    if ((double)cf > cutd) cf = std::nextafterf(cf, -INFINITY);
+    if ((double)cf > std::ldexp(cutd, sc)) cf = std::nextafterf(cf, -INFINITY);
     D.cut_tc[r] = cf;
+    D.cut_tc[kFilters + r] = (float)std::ldexp(1.0, -sc);
   }
-  TRY(D.w_tc.ensure(sizeof(float) * wtc.size()));
-  TRY(D.cuttc.ensure(sizeof(float) * kFilters));
-  CK(cudaMemcpy(D.w_tc.p, wtc.data(), sizeof(float) * wtc.size(), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(D.cuttc.p, D.cut_tc, sizeof(float) * kFilters, cudaMemcpyHostToDevice));
+  TRY(D.w_tc.ensure(sizeof(uint16_t) * wtc.size()));
+  TRY(D.cuttc.ensure(sizeof(float) * 2 * kFilters));
+  CK(cudaMemcpy(D.w_tc.p, wtc.data(), sizeof(uint16_t) * wtc.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(D.cuttc.p, D.cut_tc, sizeof(float) * 2 * kFilters, cudaMemcpyHostToDevice));
   TRY(D.w64.ensure(sizeof(double) * kFilters * kFilterW));
   TRY(D.w32.ensure(sizeof(float) * w32.size()));
   TRY(D.bias64.ensure(sizeof(double) * kFilters));
@@ -1509,10 +1534,13 @@ int bl_debug_screen_tc(bl_ctx* c, const double* features, int cw, int ch, float*
   LevelDesc& Lv = H.lv[0];
   const size_t nfl = tc_feat_floats_per_frame(cw, ch, &Lv.tc_ncp, nullptr);
   Lv.tc_off = 0;
-  std::vector<float> host(nfl, 0.f);
+  std::vector<uint16_t> h16(2 * nfl, 0);  // fp16 planes, as k_features writes them
   for (long long cell = 0; cell < (long long)cw * ch; ++cell)
     for (int f = 0; f < kFeat; ++f)
-      host[((size_t)(f / 4) * Lv.tc_ncp + cell) * 4 + f % 4] = tf32_round_host((float)features[cell * kFeat + f]);
+      h16[((size_t)(f / 8) * Lv.tc_ncp + cell) * 8 + f % 8] =
+          half_rn_host(std::ldexp(features[cell * kFeat + f], kTcFeatExp));
+  std::vector<float> host(nfl);
+  std::memcpy(host.data(), h16.data(), sizeof(float) * nfl);
   const long long na = (long long)Lv.sw * Lv.sh;
   TRY(c->s_a.ensure(sizeof(float) * nfl));
   TRY(c->s_b.ensure(sizeof(float) * kFilters * na));

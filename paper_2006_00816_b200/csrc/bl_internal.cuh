@@ -25,6 +25,10 @@ constexpr int kRowW = kWin * kFeat;  // 310 weights per window row
 constexpr int kFilterW = kWin * kRowW;  // 3100
 constexpr int kFilters = 5;
 constexpr int kMaxLevels = 32;
+// tcgen05 screen operands: fp16 chunk planes (8 features per 16-B chunk, 32 features incl. a
+// zero pad), features scaled by 2^kTcFeatExp so values below 2^-14 keep precision
+constexpr int kTcPlanesF16 = 4;
+constexpr int kTcFeatExp = 8;
 
 // Screening tile: a warp scores 128 anchors, 4 consecutive anchors along x per lane, all 5
 // filters; per level the tile is 32x4, 16x8 or 8x16 anchors, whichever wastes least.
@@ -63,7 +67,7 @@ struct LevelDesc {
                                // (4 * sc_lanes_x) x (32 / sc_lanes_x) anchors
   long long sc_begin;          // first screening warp-tile id of this level
   long long cell_begin;        // first cell id (for per-cell kernels) of this level
-  long long tc_off;            // tcgen05 screen features: float offset of frame 0 ([8 planes][tc_ncp][4])
+  long long tc_off;            // tcgen05 screen features: 4-B word offset of frame 0 ([4 planes][tc_ncp][8 fp16])
   long long tc_ncp;            // cells per plane (linear index cy * cw + cx, zero-padded tail)
   long long anchor_base;       // per-frame anchor offset (for candidate records)
 };

@@ -10,23 +10,27 @@
 // accumulated over j in TMEM, and the epilogue finishes the correlation along x:
 // score[L][r] = sum_dx Q[L + dx][dx, r] (cells L .. L+9 of the same 128-cell tile, so a tile
 // yields 119 anchors).  Putting dx into N instead of shifting A keeps every MMA at
-// M = 128, N = 64, K = 8 with a 4 KB A tile (an N = 16 per-dx formulation re-reads A from
+// M = 128, N = 64, K = 16 with a 4 KB A tile (an N = 16 per-dx formulation re-reads A from
 // shared memory ten times and is smem-bandwidth-bound).  Anchors whose cx lands in the last
 // 9 columns wrap into the next image row; they are discarded by the epilogue's
 // (cx < sw, cy < sh) test.
 //
-// Per CTA (persistent, one per SM): the tf32 weights of all 10 window rows (80 KB) stay in
-// shared memory; warp 0 streams, per (unit, j), the 8 feature planes (4 tf32 features each)
-// of the unit's cell range into a 3-stage ring with cp.async.bulk; one thread of warp 1
-// issues 4 k-steps of tcgen05.mma.kind::tf32 per m-tile into TMEM; warps 2-5 read the
-// accumulators back with tcgen05.ld (one cell per TMEM lane), do the dx-correlation through
+// Per CTA (persistent, one per SM): the fp16 weights of all 10 window rows (40 KB) stay in
+// shared memory; warp 0 streams, per unit, the 4 feature planes (8 fp16 features each) of the
+// cell band all 10 window rows read (rows overlap by all but cw cells, so the band is
+// copied once; levels wider than 80 cells take several row groups) into a 2-stage ring with
+// cp.async.bulk; one thread of warp 1 issues 2 k-steps of tcgen05.mma.kind::f16 per row and
+// m-tile into TMEM; warps 2-5 read the accumulators back with tcgen05.ld (one cell per TMEM lane), do the dx-correlation through
 // shared memory, apply the rigorous cut and append candidates.  Two TMEM accumulator sets
 // let the epilogue of unit u overlap the MMAs of unit u + 1.
 //
-// Precision: features and weights are rounded to tf32 (round-to-nearest) and the MMA
-// accumulates in fp32, so |screen - exact| <= delta_tc (bl_capi.cu: rigorous bound with
-// 2^-10 relative operand rounding plus accumulation); every candidate is re-scored exactly
-// in fp64 by bl_exact.cu, so output bits never depend on this kernel's rounding.
+// Precision: features (scaled by 2^8) and weights (scaled per filter by a power of two to
+// [2^14, 2^15)) are rounded to fp16 (round-to-nearest-even) and the MMA accumulates in fp32;
+// the power-of-two scales are exact and folded into the cut, so |screen - exact| <= delta_tc
+// (bl_capi.cu: rigorous bound with 2^-10 relative operand rounding, the fp16 subnormal floor
+// and accumulation); every candidate is re-scored exactly in fp64 by bl_exact.cu, so output
+// bits never depend on this kernel's rounding.  (fp16 vs tf32: the same 11-bit significand,
+// half the feature bytes and twice the MMA K per instruction.)
 #include "bl_internal.cuh"
 
 namespace blb {
@@ -38,23 +42,33 @@ constexpr int kTcV = kTcM - (kWin - 1);   // anchors per m-tile (119)
 constexpr int kTcN = 64;              // 10 dx x 5 filters = 50 columns, padded
 constexpr int kTcNM = 2;              // m-tiles per work unit
 constexpr int kTcNA = 248;            // cells staged per plane: kTcV * (kTcNM - 1) + kTcM, rounded to 8
-constexpr int kTcPlanes = 8;          // 32 features / 4 per 16-B chunk
+constexpr int kTcPlanes = kTcPlanesF16;  // 32 features / 8 fp16 per 16-B chunk
+constexpr int kTcKSteps = kTcPlanes / 2;  // MMAs (K = 16 = two chunks) per window row
 #ifndef BL_TC_J
-#define BL_TC_J 2
+#define BL_TC_J 10
 #endif
 constexpr int kTcJ = BL_TC_J;        // window rows per stage: their cell ranges overlap by cw
-constexpr int kTcCwMax = 80;          // levels wider than this stage one window row at a time
+constexpr int kTcCwMax = 80;          // a stage holds kTcJ rows of levels up to this wide
 constexpr int kTcNAS = kTcNA + (kTcJ - 1) * kTcCwMax;      // cells per plane per stage
-constexpr int kTcStages = kTcJ > 1 ? 2 : 3;
-constexpr int kTcABytes = kTcPlanes * kTcNAS * 16;          // 41,984 per stage (J = 2)
-constexpr int kTcWRowBytes = kTcPlanes * kTcN * 16;         // 8,192 per window row j
-constexpr int kTcWBytes = kWin * kTcWRowBytes;              // 81,920 resident
+#ifndef BL_TC_STAGES
+#define BL_TC_STAGES 2
+#endif
+constexpr int kTcStages = BL_TC_STAGES;
+constexpr int kTcABytes = kTcPlanes * kTcNAS * 16;          // 61,952 per stage (J = 10)
+constexpr int kTcWRowBytes = kTcPlanes * kTcN * 16;         // 4,096 per window row j
+constexpr int kTcWBytes = kWin * kTcWRowBytes;              // 40,960 resident
 constexpr int kTcEpiBytes = 50 * kTcM * 4;                  // 25,600: Q tile for the dx-correlation
 constexpr int kTcAccCols = kTcNM * kTcN;                    // 128 columns per accumulator set
 constexpr int kTcTmemCols = 256;                            // two sets
 constexpr int kTcThreads = 6 * 32;
 constexpr size_t kTcSmem = (size_t)kTcWBytes + kTcStages * kTcABytes + kTcEpiBytes + 1024;
 static_assert(kTcNA >= kTcV * (kTcNM - 1) + kTcM && kTcNA % 8 == 0, "stage width");
+static_assert(kTcSmem <= 227 * 1024, "shared memory");
+
+// window rows staged together for a level cw cells wide: as many as the stage holds
+__device__ __forceinline__ int rows_per_stage(int cw) {
+  return min(kTcJ, 1 + (kTcNAS - kTcNA) / max(cw, 1));
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -101,15 +115,16 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
 }
 
-// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, N = 64, M = 128.
-constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
+// kind::f16 instruction descriptor: D f32 (bits 4-5 = 1), A/B f16 (format 0), both K-major,
+// N = 64, M = 128.
+constexpr uint32_t kTcIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
                               ((uint32_t)(kTcM >> 4) << 24);
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(kTcIdesc), "r"(accumulate));
 }
 
@@ -205,7 +220,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_screen_tc(const PlanDesc* __r
         const LevelDesc& D = P->lv[s];
         const long long ncp = D.tc_ncp;
         const float* fbase = feat_tc + D.tc_off + (long long)f * kTcPlanes * ncp * 4;
-        const int jpl = D.cw <= kTcCwMax ? kTcJ : 1;
+        const int jpl = rows_per_stage(D.cw);
         for (int j0 = 0; j0 < kWin; j0 += jpl) {
           // window rows j0 .. j0+J-1 read cells [L0 + j0*cw, L0 + (j0+J-1)*cw + NA): one copy
           const int J = min(jpl, kWin - j0);
@@ -238,7 +253,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_screen_tc(const PlanDesc* __r
       long long uL0;
       unit_info(u, us, uf, uL0);
       const int cw = P->lv[us].cw;
-      const int jpl = cw <= kTcCwMax ? kTcJ : 1;
+      const int jpl = rows_per_stage(cw);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d0 = tmem_base + acc * kTcAccCols;
@@ -252,7 +267,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_screen_tc(const PlanDesc* __r
           for (int jj = 0; jj < J; ++jj) {
             const int j = j0 + jj;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
+            for (int kk = 0; kk < kTcKSteps; ++kk) {
               // B (weights of row j): [kc][64 n][16 B]: K chunk step 1024 B, 8-row group step 128 B
               const uint64_t db = umma_desc(sw0 + j * kTcWRowBytes + (2 * kk) * (kTcN * 16), kTcN * 16, 128);
 #pragma unroll
@@ -260,7 +275,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_screen_tc(const PlanDesc* __r
                 // A (cells of row j): [kc][NAS cells][16 B], row j starts jj*cw cells into the stage
                 const uint64_t da = umma_desc(sa + (uint32_t)(((2 * kk) * kTcNAS + jj * cw + m * kTcV) * 16),
                                               kTcNAS * 16, 128);
-                mma_tf32(d0 + m * kTcN, da, db, (j | kk) != 0);
+                mma_f16(d0 + m * kTcN, da, db, (j | kk) != 0);
               }
             }
           }
@@ -284,9 +299,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_screen_tc(const PlanDesc* __r
     const int t = 32 * q + lane;  // cell (TMEM lane) within the m-tile
     int acc = 0;
     uint32_t acc_phase = 0;
-    float cutv[kFilters];
+    float cutv[kFilters], unscale[kFilters];  // cut in the scaled domain; 2^-(scale exponents)
 #pragma unroll
-    for (int r = 0; r < kFilters; ++r) cutv[r] = __ldg(cut + r);
+    for (int r = 0; r < kFilters; ++r) {
+      cutv[r] = __ldg(cut + r);
+      unscale[r] = __ldg(cut + kFilters + r);
+    }
     for (long long u = blockIdx.x; u < total; u += gridDim.x) {
       int s, f;
       long long L0;
@@ -324,7 +342,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_screen_tc(const PlanDesc* __r
         const bool ok = t < kTcV && cx < D.sw && cy < D.sh;
         if (dbg_scores && ok) {
 #pragma unroll
-          for (int r = 0; r < kFilters; ++r) dbg_scores[((long long)r * D.sh + cy) * D.sw + cx] = v[r];
+          for (int r = 0; r < kFilters; ++r) dbg_scores[((long long)r * D.sh + cy) * D.sw + cx] = v[r] * unscale[r];
         }
         unsigned flags = 0;
 #pragma unroll

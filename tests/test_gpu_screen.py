@@ -34,8 +34,27 @@ def test_tc_screen_within_bound(ctx, oracle, cw, ch, seed):
         err = np.abs(tc[k].astype(np.float64) - exact)
         assert np.all(np.isfinite(tc[k]))
         assert err.max() <= delta[k], (k, err.max(), delta[k])
-        # the bound is not vacuous: tf32 error is well inside it but clearly above fp32 noise
+        # the bound is not vacuous: the fp16 operand error is well inside it
         assert err.max() < 0.5 * delta[k]
+
+
+def test_tc_screen_wide_weight_range(ctx, oracle):
+    """Weights spanning 1e-9 .. 1 in one filter and a filter of tiny weights: after the
+    per-filter power-of-two scaling the smallest land in the fp16 subnormal range, which the
+    bound covers with its absolute term."""
+    r = np.random.default_rng(31)
+    w = np.sign(r.uniform(-1, 1, (5, 3100))) * np.exp(r.uniform(np.log(1e-9), 0.0, (5, 3100)))
+    w[3] *= 1e-7
+    w[4] *= 3e4
+    model = {"weights": w, "biases": r.uniform(-1, 1, 5), "threshold": 0.0}
+    ctx.upload_detector(model)
+    feat = _features(r, 30, 40)
+    feat[..., 7] = r.uniform(0, 1e-6, (30, 40))  # features in the fp16 subnormal range too
+    tc, delta = ctx.debug_screen_tc(feat)
+    for k in range(5):
+        exact = oracle.score_separable(feat, w[k], 0.0)
+        err = np.abs(tc[k].astype(np.float64) - exact)
+        assert err.max() <= delta[k], (k, err.max(), delta[k])
 
 
 def test_tc_screen_zero_and_single_weight(ctx, oracle):
