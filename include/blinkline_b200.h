@@ -100,7 +100,7 @@ int bl_ctx_stage_times(bl_ctx* ctx, float* ms /* BL_STAGE_COUNT */, int* launche
 int bl_ctx_enable_graphs(bl_ctx* ctx, int enable);
 /* Classifier screen implementation (both feed the same exact fp64 re-score, so detections
  * are bit-identical either way): BL_SCREEN_TCGEN05 -- implicit GEMM on the tensor cores
- * (tcgen05.mma kind::tf32, default); BL_SCREEN_FP32 -- register-tiled CUDA-core FMA.  The
+ * (tcgen05.mma kind::f16, default); BL_SCREEN_FP32 -- register-tiled CUDA-core FMA.  The
  * environment variable BL_SCREEN=fp32|tc overrides the default at context creation. */
 #define BL_SCREEN_TCGEN05 0
 #define BL_SCREEN_FP32 1
