@@ -1138,10 +1138,15 @@ int bl_ert_upload(bl_ctx* c, int L, int T, int K, int F, double shrinkage, const
       }
   TRY(E.mean.ensure(sizeof(double) * 2 * L));
   TRY(E.mean_c.ensure(sizeof(double) * 2 * L));
-  TRY(E.split.ensure(sizeof(SplitRec) * recs.size()));
+  // split planes: a warp's 32 consecutive trees at one node read 3 x 512 contiguous bytes
+  const size_t plane = recs.size();
+  std::vector<int4> planes(3 * plane);
+  for (size_t i = 0; i < plane; ++i)
+    for (int q = 0; q < 3; ++q) std::memcpy(&planes[q * plane + i], reinterpret_cast<const char*>(&recs[i]) + 16 * q, 16);
+  TRY(E.split.ensure(sizeof(int4) * planes.size()));
   TRY(E.leaves.ensure(sizeof(double) * (size_t)T * K * NL * L * 2 + 16));
   CK(cudaMemcpy(E.mean.p, mean_xy, sizeof(double) * 2 * L, cudaMemcpyDefault));
-  CK(cudaMemcpy(E.split.p, recs.data(), sizeof(SplitRec) * recs.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(E.split.p, planes.data(), sizeof(int4) * planes.size(), cudaMemcpyHostToDevice));
   if ((size_t)T * K) CK(cudaMemcpy(E.leaves.p, leaves, sizeof(double) * (size_t)T * K * NL * L * 2, cudaMemcpyDefault));
   // centroid of the mean shape in similarity_transform's order (ert.cpp:33-43), and the
   // centred mean (to.x - mt.x, to.y - mt.y) every level reuses
@@ -1170,6 +1175,7 @@ int bl_ert_upload(bl_ctx* c, int L, int T, int K, int F, double shrinkage, const
   E.dev.mean_xy = E.mean.as<double>();
   E.dev.mean_c = E.mean_c.as<double>();
   E.dev.split = E.split.as<SplitRec>();
+  E.dev.split_plane = (long long)plane;
   E.dev.leaves = E.leaves.as<double>();
   E.dev.mean_cx = mx;
   E.dev.mean_cy = my;

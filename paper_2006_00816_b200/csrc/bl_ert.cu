@@ -138,14 +138,14 @@ __global__ void __launch_bounds__(256) k_ert_traverse(ErtDev M, int t, const voi
   const int* bx = boxes + (long long)face * box_stride;
   const int X = bx[0], Y = bx[1], W = bx[2], H = bx[3];
   const void* fr = (const char*)frames + (long long)face_frame[face] * fstride * (U8 ? 1 : 8);
-  const SplitRec* lvl = M.split + (long long)t * S * K;
+  const int4* lvl = reinterpret_cast<const int4*>(M.split) + (long long)t * S * K;
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     int node = 0;
     while (node < S) {
-      const SplitRec* r = lvl + (long long)node * K + k;
-      const double2 oa = __ldg(reinterpret_cast<const double2*>(r));      // offset_a
-      const double2 ob = __ldg(reinterpret_cast<const double2*>(r) + 1);  // offset_b
-      const int4 tail = __ldg(reinterpret_cast<const int4*>(r) + 2);      // thr, anchors
+      const int4* r = lvl + (long long)node * K + k;
+      const double2 oa = __ldg(reinterpret_cast<const double2*>(r));                  // offset_a
+      const double2 ob = __ldg(reinterpret_cast<const double2*>(r + M.split_plane));  // offset_b
+      const int4 tail = __ldg(r + 2 * M.split_plane);                                 // thr, anchors
       const double thr = __hiloint2double(tail.y, tail.x);
       const int an_a = (short)(tail.z & 0xffff), an_b = (short)(tail.z >> 16);
       const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_a, oa.x, oa.y);
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
     __syncthreads();
     // (2) traversals: two (face, tree) items per thread walk their trees in lock-step (all
     // trees have depth F), so each level's record and pixel loads of both are in flight together
-    const SplitRec* lvl = M.split + (long long)t * S * K;
+    const int4* lvl = reinterpret_cast<const int4*>(M.split) + (long long)t * S * K;
     const int items = nf * K;
     for (int e0 = tid; e0 < items; e0 += 2 * blockDim.x) {
       const int e1 = min(e0 + (int)blockDim.x, items - 1);  // a duplicate of e0's last item when odd
@@ -294,10 +294,10 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
       for (int d = 0; d < M.F; ++d) {
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const SplitRec* r = lvl + (long long)it[q].node * K + it[q].k;
+          const int4* r = lvl + (long long)it[q].node * K + it[q].k;
           const double2 oa = __ldg(reinterpret_cast<const double2*>(r));
-          const double2 ob = __ldg(reinterpret_cast<const double2*>(r) + 1);
-          const int4 tail = __ldg(reinterpret_cast<const int4*>(r) + 2);
+          const double2 ob = __ldg(reinterpret_cast<const double2*>(r + M.split_plane));
+          const int4 tail = __ldg(r + 2 * M.split_plane);
           const double thr = __hiloint2double(tail.y, tail.x);
           const int an_a = (short)(tail.z & 0xffff), an_b = (short)(tail.z >> 16);
           const double* cur = sc + it[q].fi * L2;

@@ -155,7 +155,8 @@ struct ErtDev {
   double shrinkage;
   const double* mean_xy;      // L*2
   const double* mean_c;       // L*2: mean shape minus its centroid (ert.cpp:41-46 txp/typ)
-  const SplitRec* split;      // [T][S][K]
+  const SplitRec* split;      // 3 planes of 16-B entries [T][S][K]: (oax, oay), (obx, oby), (thr, anchors)
+  long long split_plane;      // entries per plane
   const double* leaves;       // T*K*NL*L*2
   double mean_cx, mean_cy;    // centroid of the mean shape (host-computed, ert.cpp:33-43 order)
 };
