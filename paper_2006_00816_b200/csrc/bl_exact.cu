@@ -49,7 +49,10 @@ BL_DEV int round_half_up(double v) { return (int)floor(dadd(v, 0.5)); }  // dete
 // the strips cross L1 once per anchor rather than once per (anchor, filter).
 constexpr int kRsPitch = 33;
 constexpr int kRsWPitch = kRowW + 1;  // 311
-constexpr int kRsWarps = 8;
+#ifndef BL_RS_WARPS
+#define BL_RS_WARPS 6
+#endif
+constexpr int kRsWarps = BL_RS_WARPS;
 constexpr int kRsWarpDoubles = 30 * kRsPitch;
 constexpr size_t kRsSmem =
     sizeof(double) * ((size_t)kRsWarps * kRsWarpDoubles + (size_t)kFilters * kWin * kRsWPitch);
