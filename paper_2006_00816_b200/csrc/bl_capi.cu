@@ -118,6 +118,8 @@ constexpr int kLevelMargin = 8;  // readable doubles either side of every arena 
 uint16_t half_rn_host(double x) {
   const uint16_t sign = std::signbit(x) ? 0x8000 : 0;
   const double a = std::fabs(x);
+  if (std::isnan(x)) return 0x7e00;
+  if (a >= 65520.0) return (uint16_t)(sign | 0x7c00);  // rounds to infinity
   if (a == 0.0) return sign;
   int e = 0;
   std::frexp(a, &e);  // a = m 2^e, m in [0.5, 1): binade exponent e - 1
@@ -1061,7 +1063,7 @@ int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, d
     for (int k = 0; k < kFilterW; ++k) mx = std::max(mx, std::fabs(weights[(size_t)r * kFilterW + k]));
     int e = 0;
     if (mx > 0) std::frexp(mx, &e);       // mx in [2^(e-1), 2^e)
-    ws[r] = mx > 0 ? 15 - e : 0;          // mx * 2^ws in [2^14, 2^15)
+    ws[r] = mx > 0 && std::isfinite(mx) ? 15 - e : 0;  // mx * 2^ws in [2^14, 2^15)
     ws[r] = std::max(-100, std::min(100, ws[r]));
   }
   std::vector<uint16_t> wtc(tc_weight_floats() * 2, 0);
