@@ -107,3 +107,20 @@ def test_screens_agree_with_oracle_pattern(ctx, oracle, pattern_model):
 def test_screen_mode_validation(ctx):
     with pytest.raises(Exception):
         ctx.set_screen("bf16")
+
+
+def test_screens_non_finite_weights(ctx, oracle, pattern_model):
+    """A NaN or infinite weight makes that filter's scores NaN / +-inf in the reference; the
+    screen then cannot bound its error (delta = inf, every anchor nominated) and the exact
+    re-score decides exactly as the reference does."""
+    from pyoracle import ring_frames_np
+    m = {k: (np.array(v, copy=True) if isinstance(v, np.ndarray) else v) for k, v in pattern_model.items()}
+    m["weights"] = np.array(m["weights"], dtype=np.float64, copy=True)
+    m["weights"][2, 17] = np.nan
+    m["weights"][3, 1000] = np.inf
+    frames = ring_frames_np(2, 320, 240, seed=12)
+    got = _detect_both(ctx, frames, m)
+    for i in range(len(frames)):
+        want = oracle.detect_faces(frames[i].astype(np.float64), m)
+        assert np.array_equal(got["tc"][i], want)
+        assert np.array_equal(got["fp32"][i], want)
