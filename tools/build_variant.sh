@@ -1,7 +1,7 @@
 #!/bin/bash
 # Build an experimental variant of libblinkline_b200.so with extra -D flags into
 # variants/NAME/ (git-ignored; travels to the GPU box).  Select it with BL_LIBRARY.
-#   bash tools/build_variant.sh NAME "-DBL_HOG_BATCH=1 -DBL_HOG_MINBLOCKS=5"
+#   bash tools/build_variant.sh NAME "-DBL_HOG_SEG=16 -DBL_TC_STAGES=3"
 set -e
 NAME=$1; DEFS=$2
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
