@@ -1,3 +1,6 @@
+#!/bin/bash
+# GPU box: short device-resident bench of the main build and every variants/*/ build.
+#   gpurun -- 'bash tools/bench_variants.sh'
 run() { timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > /tmp/o.json 2> /tmp/o.err; python -c "
 import json,sys
 try:
