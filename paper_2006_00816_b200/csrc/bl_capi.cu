@@ -237,7 +237,9 @@ struct bl_ctx {
   uint64_t next_ticket = 1;
   int face_cap_per_frame = 64;  // device-side capacity of landmarked faces per frame
   int screen = BL_SCREEN_TCGEN05;
-  bool ert_fused = true;  // BL_ERT=levels selects the per-level kernels (experiments)
+  // landmark cascade kernel: auto (k_ert_wide for small batches, else k_ert_cascade), or forced
+  // by BL_ERT=wide|cascade|levels (experiments)
+  int ert_mode = 0;
 };
 
 namespace {
@@ -537,9 +539,14 @@ int check_frames(const void* frames, int pix, int n, int w, int h, size_t pitch,
 
 // Runs the ERT cascade for `nf` faces whose boxes (int stride) and frame indices are on the
 // device; n_faces_dev holds the count.  Output landmarks -> c->ert_out.
+// Face-count threshold of the wide (face-per-CTA) cascade, and the per-frame face estimate a
+// streamed batch is judged by before its detections exist (the count stays on the device).
+constexpr long long kErtWideMaxFaces = 400;  // measured crossover 300-600 faces (tools/diag_ert_wide.py)
+constexpr long long kErtFacesPerFrameGuess = 4;
+
 int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix, int w, int h, long long pitch,
             long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces_dev,
-            int nf, uint8_t* leaf_dev, double* out_xy, int* err_dev) {
+            int nf, uint8_t* leaf_dev, double* out_xy, int* err_dev, long long expect_faces) {
   ErtState& E = c->ert;
   const Launch L{st, &c->launches};
   const int L2 = 2 * E.dev.L;
@@ -554,7 +561,15 @@ int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix
     leaf = wk.leafs.as<uint8_t>();
   }
   CK(cudaMemsetAsync(err_dev, 0, sizeof(int), st));
-  if (c->ert_fused && ert_cascade_fits(E.dev)) {  // one launch for the whole cascade
+  // one launch for the whole cascade: a face per CTA while the batch is too small to fill the
+  // GPU with kFcFaces-face CTAs (latency), else kFcFaces faces per CTA (leaf-row reuse in L1)
+  const bool wide = c->ert_mode == 2 || (c->ert_mode == 0 && expect_faces <= kErtWideMaxFaces);
+  if (wide && ert_wide_fits(E.dev)) {
+    launch_ert_wide(L, E.dev, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
+                    n_faces_dev, nf, out_xy, leaf_dev, (long long)E.dev.T * E.dev.K, err_dev);
+    return BL_OK;
+  }
+  if (c->ert_mode != 3 && ert_cascade_fits(E.dev)) {
     launch_ert_cascade(L, E.dev, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
                        n_faces_dev, nf, out_xy, leaf_dev, (long long)E.dev.T * E.dev.K, err_dev);
     return BL_OK;
@@ -667,7 +682,7 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
       CK(cudaStreamWaitEvent(es, S.ev_det, 0));
     }
     TRY(run_ert(c, es, S.ert, dev, pix, w, h, dp, df, S.face_frame.as<int>(), S.flat.as<int>(), 8, meta + n,
-                (int)cap_faces, nullptr, S.ert_out.as<double>(), meta + n + 2));
+                (int)cap_faces, nullptr, S.ert_out.as<double>(), meta + n + 2, (long long)n * kErtFacesPerFrameGuess));
     CK(cudaEventRecord(S.ev_done, es));
   } else {
     CK(cudaMemsetAsync(meta + n + 2, 0, sizeof(int), c->st));
@@ -916,7 +931,8 @@ int bl_ctx_create(int device, bl_ctx** out) {
   }
   set_direction_table(ux, uy);
   if (const char* e = std::getenv("BL_SCREEN")) c->screen = std::strcmp(e, "fp32") == 0 ? BL_SCREEN_FP32 : BL_SCREEN_TCGEN05;
-  if (const char* e = std::getenv("BL_ERT")) c->ert_fused = std::strcmp(e, "levels") != 0;
+  if (const char* e = std::getenv("BL_ERT"))
+    c->ert_mode = !std::strcmp(e, "cascade") ? 1 : !std::strcmp(e, "wide") ? 2 : !std::strcmp(e, "levels") ? 3 : 0;
   CK(cudaGetLastError());
   *out = c.release();
   return BL_OK;
@@ -1286,7 +1302,7 @@ int bl_landmarks(bl_ctx* c, const void* frames, int pixel_type, int n_frames, in
   TRY(c->ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * std::max(1, nf)));
   TRY(c->ert_err.ensure(sizeof(int)));
   TRY(run_ert(c, c->st, c->ert_work, dev, pixel_type, w, h, dp, df, c->ert_frames.as<int>(), c->ert_boxes.as<int>(), 4,
-              c->ert_nfaces.as<int>(), nf, leaf_dev, c->ert_out.as<double>(), c->ert_err.as<int>()));
+              c->ert_nfaces.as<int>(), nf, leaf_dev, c->ert_out.as<double>(), c->ert_err.as<int>(), nf));
   stage_mark(c, BL_STAGE_D2H);
   CK(cudaMemcpyAsync(out_xy, c->ert_out.p, sizeof(double) * 2 * c->ert.dev.L * n_boxes, cudaMemcpyDefault, c->st));
   if (leaf_idx)

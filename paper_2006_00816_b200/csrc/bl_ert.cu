@@ -17,6 +17,8 @@
 // once per batch; L2 serves the 1088-B leaf row each (face, tree) selects.
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "bl_internal.cuh"
 
 namespace blb {
@@ -353,6 +355,120 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
     out_xy[(long long)(f0 + fi) * L2 + c] = (c & 1) ? dadd((double)b[1], dmul(sc[e], (double)b[3]))
                                                     : dadd((double)b[0], dmul(sc[e], (double)b[2]));
   }
+}
+
+// The cascade for SMALL batches (a camera stream's 16 frames, one frame): one face per CTA
+// and a thread per tree / per coordinate, so a level's latency chain is one traversal and
+// one K-long sum instead of kFcFaces faces' worth of them per thread.  Same arithmetic as
+// k_ert_cascade (bit-identical):
+//   xform    thread 0: similarity transform of the staged current shape;
+//   traverse thread per tree: level-order descent, leaf index -> smem;
+//   accum    thread per coordinate: the K selected leaf values in tree order, 32 loads in
+//            flight, cur += shrinkage * delta.
+#ifndef BL_ERT_WIDE_THREADS
+#define BL_ERT_WIDE_THREADS 256
+#endif
+constexpr int kWdThreads = BL_ERT_WIDE_THREADS;
+
+template <bool U8>
+__global__ void __launch_bounds__(kWdThreads) k_ert_wide(ErtDev M, const void* __restrict__ frames, int w, int h,
+                                                  long long pitch, long long fstride,
+                                                  const int* __restrict__ face_frame,
+                                                  const int* __restrict__ boxes, int box_stride,
+                                                  const int* __restrict__ n_faces, int cap,
+                                                  double* __restrict__ out_xy, uint8_t* __restrict__ leaf_out,
+                                                  long long leaf_out_stride, int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char wd_smem[];
+  const int L = M.L, L2 = 2 * L, K = M.K, S = M.S, NL = M.NL;
+  double* sc = reinterpret_cast<double*>(wd_smem);             // [2L]
+  double2* stf = reinterpret_cast<double2*>(sc + L2);          // [1]
+  uint8_t* sli = reinterpret_cast<uint8_t*>(stf + 1);          // [K]
+  const int n = min(*n_faces, cap);
+  const int face = blockIdx.x;
+  if (face >= n) return;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < L2; e += blockDim.x) sc[e] = M.mean_xy[e];  // ert.cpp:106
+  const int* bx = boxes + (long long)face * box_stride;
+  const int X = bx[0], Y = bx[1], W = bx[2], H = bx[3];
+  const void* fr = (const char*)frames + (long long)face_frame[face] * fstride * (U8 ? 1 : 8);
+  __syncthreads();
+  for (int t = 0; t < M.T; ++t) {
+    if (tid == 0) {  // (1) transform
+      double A, B;
+      const int e = face_transform(M, sc, A, B);
+      if (e) atomicExch(err, e);
+      stf[0] = make_double2(A, B);
+    }
+    __syncthreads();
+    // (2) traversals, ert.cpp:87-97
+    const double2 ab = stf[0];
+    const int4* lvl = reinterpret_cast<const int4*>(M.split) + (long long)t * S * K;
+    for (int k = tid; k < K; k += blockDim.x) {
+      int node = 0;
+      for (int d = 0; d < M.F; ++d) {
+        const int4* r = lvl + (long long)node * K + k;
+        const double2 oa = __ldg(reinterpret_cast<const double2*>(r));
+        const double2 ob = __ldg(reinterpret_cast<const double2*>(r + M.split_plane));
+        const int4 tail = __ldg(r + 2 * M.split_plane);
+        const double thr = __hiloint2double(tail.y, tail.x);
+        const int an_a = (short)(tail.z & 0xffff), an_b = (short)(tail.z >> 16);
+        const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_a, oa.x, oa.y);
+        const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_b, ob.x, ob.y);
+        node = dsub(ia, ib) > thr ? 2 * node + 1 : 2 * node + 2;
+      }
+      sli[k] = (uint8_t)(node - S);
+      if (leaf_out) leaf_out[(long long)face * leaf_out_stride + (long long)t * K + k] = (uint8_t)(node - S);
+    }
+    __syncthreads();
+    // (3) leaf sums in tree order, cur += shrinkage * delta (ert.cpp:118-126)
+    if (tid < L2) {
+      double acc = 0.0;
+      const double* lv = M.leaves + (long long)t * K * NL * L2 + tid;
+      const int row = NL * L2;
+      int k = 0;
+      for (; k + 32 <= K; k += 32) {
+        double v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v[u] = __ldg(lv + (long long)(k + u) * row + sli[k + u] * L2);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) acc = dadd(acc, v[u]);
+      }
+      for (; k < K; ++k) acc = dadd(acc, __ldg(lv + (long long)k * row + sli[k] * L2));
+      sc[tid] = dadd(sc[tid], dmul(M.shrinkage, acc));  // the traversals' reads of sc are done
+    }
+    __syncthreads();
+  }
+  // ert.cpp:132-133: box.x + p.x * box.w, box.y + p.y * box.h
+  for (int c = tid; c < L2; c += blockDim.x)
+    out_xy[(long long)face * L2 + c] = (c & 1) ? dadd((double)Y, dmul(sc[c], (double)H))
+                                               : dadd((double)X, dmul(sc[c], (double)W));
+}
+
+bool ert_wide_fits(const ErtDev& M) { return 2 * M.L <= kWdThreads && 2 * M.L <= kMaxL2; }
+
+void launch_ert_wide(const Launch& L, const ErtDev& M, const void* frames, int u8, int w, int h, long long pitch,
+                     long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces,
+                     int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err) {
+  const size_t smem = sizeof(double) * 2 * M.L + sizeof(double2) + (size_t)M.K;
+  static size_t attr_u8 = 0, attr_f64 = 0;
+  size_t& attr = u8 ? attr_u8 : attr_f64;
+  if (smem > 48 * 1024 && smem > attr) {
+    if (u8)
+      cudaFuncSetAttribute(k_ert_wide<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else
+      cudaFuncSetAttribute(k_ert_wide<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  const int threads = (int)std::min<long long>(kWdThreads, std::max<long long>(div_up(M.K, 32), div_up(2 * M.L, 32)) * 32);
+  if (u8)
+    k_ert_wide<true><<<(unsigned)cap, threads, smem, L.st>>>(M, frames, w, h, pitch, fstride, face_frame, boxes,
+                                                              box_stride, n_faces, cap, out_xy, leaf_out,
+                                                              leaf_out_stride, err);
+  else
+    k_ert_wide<false><<<(unsigned)cap, threads, smem, L.st>>>(M, frames, w, h, pitch, fstride, face_frame, boxes,
+                                                               box_stride, n_faces, cap, out_xy, leaf_out,
+                                                               leaf_out_stride, err);
+  ++*L.counter;
 }
 
 bool ert_cascade_fits(const ErtDev& M) {

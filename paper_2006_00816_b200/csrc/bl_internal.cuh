@@ -227,6 +227,10 @@ void launch_ert_level(const Launch& L, const ErtDev& M, int t, const void* frame
                       const int* n_faces, int cap, double* cur, double2* tf, uint8_t* leaf_idx,
                       long long leaf_stride, int* err);
 bool ert_cascade_fits(const ErtDev& M);
+bool ert_wide_fits(const ErtDev& M);
+void launch_ert_wide(const Launch& L, const ErtDev& M, const void* frames, int u8, int w, int h, long long pitch,
+                     long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces,
+                     int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err);
 void launch_ert_cascade(const Launch& L, const ErtDev& M, const void* frames, int u8, int w, int h, long long pitch,
                         long long fstride, const int* face_frame, const int* boxes, int box_stride,
                         const int* n_faces, int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride,

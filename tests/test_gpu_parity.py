@@ -336,6 +336,32 @@ def test_ert_random_vs_oracle(ctx, oracle):
     assert mism == 0
 
 
+@pytest.mark.parametrize("n", [3, 450])
+def test_ert_wide_and_cascade_kernels_agree(monkeypatch, oracle, n):
+    """k_ert_wide (face per CTA, small batches) and k_ert_cascade (4 faces per CTA) are the same
+    arithmetic: bit-identical landmarks and leaves, both against the oracle."""
+    import paper_2006_00816_b200 as bl
+    from pyoracle import random_ert
+    ert = random_ert(T=3, K=40, F=4, seed=11)
+    img = np.floor(rng(12).uniform(0, 256, (240, 320)))
+    r = rng(13)
+    boxes = np.stack([r.integers(-20, 260, n), r.integers(-20, 180, n), r.integers(30, 160, n),
+                      r.integers(30, 160, n)], axis=1).astype(np.int32)
+    out = {}
+    for mode in ("wide", "cascade"):
+        monkeypatch.setenv("BL_ERT", mode)
+        c = bl.Context(0)
+        c.upload_ert(ert)
+        out[mode] = c.landmarks(img.astype(np.uint8), np.zeros(n, np.int32), boxes, want_leaves=True)
+        c.close()
+    assert np.array_equal(out["wide"][0], out["cascade"][0])
+    assert np.array_equal(out["wide"][1], out["cascade"][1])
+    for i in range(0, n, max(1, n // 8)):
+        wxy, wl, _ = oracle.predict_landmarks(img, tuple(boxes[i]), ert)
+        assert np.array_equal(out["wide"][1][i], wl)
+        assert np.max(np.abs(out["wide"][0][i] - wxy)) <= 1e-9
+
+
 def test_ert_zero_delta_is_mean_shape(ctx):
     from pyoracle import face68_mean_shape_np
     mean = face68_mean_shape_np()
