@@ -16,6 +16,7 @@
 // trees, depth 4, L = 68) resident in L2 for every face of the batch: HBM reads the model
 // once per batch; L2 serves the 1088-B leaf row each (face, tree) selects.
 #include <stdint.h>
+#include <stdio.h>
 
 #include <algorithm>
 
@@ -54,7 +55,7 @@ BL_DEV double sample_px(const void* fr, int w, int h, long long pitch, int bx, i
   return __ldg((const double*)fr + (long long)iy * pitch + ix);
 }
 
-__device__ int face_transform(const ErtDev& M, const double* c, double& A, double& B);
+__device__ int face_transform(const ErtDev& M, const double* c, double& A, double& B, const double* mc = nullptr);
 
 // (1) similarity_transform(current, mean) per face, ert.cpp:26-69.  A warp per face stages
 // the current shape in shared memory; lane 0 then runs the sums sequentially in the
@@ -85,9 +86,11 @@ __global__ void __launch_bounds__(32 * kXfFaces) k_ert_xform(ErtDev M, const int
 // similarity_transform(current -> mean) of one face (ert.cpp:26-69), sequential sums in the
 // reference's order; returns 0 or the reference's error (1: source shape has no spread, 2:
 // target shape has no spread) and the linear part (scale*cos, scale*sin) in A, B.
-__device__ int face_transform(const ErtDev& M, const double* c, double& A, double& B) {
+// `mc`: a shared-memory copy of M.mean_c (else read through the read-only path).
+__device__ int face_transform(const ErtDev& M, const double* c, double& A, double& B, const double* mc) {
   const int L = M.L;
   double mfx = 0.0, mfy = 0.0;
+#pragma unroll 4
   for (int i = 0; i < L; ++i) {
     mfx = dadd(mfx, c[2 * i]);
     mfy = dadd(mfy, c[2 * i + 1]);
@@ -95,11 +98,13 @@ __device__ int face_transform(const ErtDev& M, const double* c, double& A, doubl
   mfx = ddiv(mfx, (double)L);
   mfy = ddiv(mfy, (double)L);
   double sff = 0.0, sre = 0.0, sim = 0.0;
+#pragma unroll 4
   for (int i = 0; i < L; ++i) {
     const double fx = dsub(c[2 * i], mfx);
     const double fy = dsub(c[2 * i + 1], mfy);
-    const double txp = __ldg(M.mean_c + 2 * i);  // to.x - mt.x, host-computed with the same op
-    const double typ = __ldg(M.mean_c + 2 * i + 1);
+    // to.x - mt.x, host-computed with the same op
+    const double txp = mc ? mc[2 * i] : __ldg(M.mean_c + 2 * i);
+    const double typ = mc ? mc[2 * i + 1] : __ldg(M.mean_c + 2 * i + 1);
     sff = dadd(sff, dadd(dmul(fx, fx), dmul(fy, fy)));
     sre = dadd(sre, dadd(dmul(fx, txp), dmul(fy, typ)));
     sim = dadd(sim, dsub(dmul(fx, typ), dmul(fy, txp)));
@@ -369,6 +374,23 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
 #define BL_ERT_WIDE_THREADS 256
 #endif
 constexpr int kWdThreads = BL_ERT_WIDE_THREADS;
+#ifndef BL_WD_PROBE
+#define BL_WD_PROBE 0  // timing probes: bit 0 skips the sums, 1 the traversals, 2 the transform
+#endif
+
+#ifndef BL_WD_CLOCK
+#define BL_WD_CLOCK 0  // per-phase clock64 totals of face 0, printed (experiments)
+#endif
+
+#ifndef BL_WD_INFLIGHT
+#define BL_WD_INFLIGHT 32
+#endif
+constexpr int kWdInFlight = BL_WD_INFLIGHT;  // leaf loads in flight per coordinate thread
+
+struct SplitPlanes {  // one split record as its three 16-B planes
+  double2 oa, ob;
+  int4 tail;  // thr (lo, hi), anchors (a | b << 16)
+};
 
 template <bool U8>
 __global__ void __launch_bounds__(kWdThreads) k_ert_wide(ErtDev M, const void* __restrict__ frames, int w, int h,
@@ -381,63 +403,103 @@ __global__ void __launch_bounds__(kWdThreads) k_ert_wide(ErtDev M, const void* _
   extern __shared__ __align__(16) unsigned char wd_smem[];
   const int L = M.L, L2 = 2 * L, K = M.K, S = M.S, NL = M.NL;
   double* sc = reinterpret_cast<double*>(wd_smem);             // [2L]
-  double2* stf = reinterpret_cast<double2*>(sc + L2);          // [1]
+  double* smc = sc + L2;                                       // [2L] mean_c
+  double2* stf = reinterpret_cast<double2*>(smc + L2);         // [1]
   uint8_t* sli = reinterpret_cast<uint8_t*>(stf + 1);          // [K]
+  const int bd = blockDim.x;
   const int n = min(*n_faces, cap);
   const int face = blockIdx.x;
   if (face >= n) return;
   const int tid = threadIdx.x;
-  for (int e = tid; e < L2; e += blockDim.x) sc[e] = M.mean_xy[e];  // ert.cpp:106
+  for (int e = tid; e < L2; e += blockDim.x) {
+    sc[e] = M.mean_xy[e];  // ert.cpp:106
+    smc[e] = M.mean_c[e];
+  }
   const int* bx = boxes + (long long)face * box_stride;
   const int X = bx[0], Y = bx[1], W = bx[2], H = bx[3];
   const void* fr = (const char*)frames + (long long)face_frame[face] * fstride * (U8 ? 1 : 8);
   __syncthreads();
+#if BL_WD_CLOCK
+  long long clk[3] = {0, 0, 0};
+#endif
   for (int t = 0; t < M.T; ++t) {
-    if (tid == 0) {  // (1) transform
+    const int4* lvl = reinterpret_cast<const int4*>(M.split) + (long long)t * S * K;
+    auto rec = [&](int node, int k, SplitPlanes& r) {
+      const int4* q = lvl + (long long)node * K + k;
+      r.oa = __ldg(reinterpret_cast<const double2*>(q));
+      r.ob = __ldg(reinterpret_cast<const double2*>(q + M.split_plane));
+      r.tail = __ldg(q + 2 * M.split_plane);
+    };
+#if BL_WD_CLOCK
+    long long c0 = clock64();
+#endif
+    if (tid == 0 && !(BL_WD_PROBE & 4)) {  // (1) transform
       double A, B;
-      const int e = face_transform(M, sc, A, B);
+      const int e = face_transform(M, sc, A, B, smc);
       if (e) atomicExch(err, e);
       stf[0] = make_double2(A, B);
     }
     __syncthreads();
-    // (2) traversals, ert.cpp:87-97
+#if BL_WD_CLOCK
+    long long c1 = clock64();
+#endif
+    // (2) traversals, ert.cpp:87-97: two trees per thread walked in lock-step (all trees
+    // have depth F), so both trees' record and pixel loads are in flight together
     const double2 ab = stf[0];
-    const int4* lvl = reinterpret_cast<const int4*>(M.split) + (long long)t * S * K;
-    for (int k = tid; k < K; k += blockDim.x) {
-      int node = 0;
+    for (int k0 = tid; k0 < K && !(BL_WD_PROBE & 2); k0 += 2 * bd) {
+      const int kk[2] = {k0, k0 + bd < K ? k0 + bd : k0};  // a duplicate of k0 when unpaired
+      int node[2] = {0, 0};
       for (int d = 0; d < M.F; ++d) {
-        const int4* r = lvl + (long long)node * K + k;
-        const double2 oa = __ldg(reinterpret_cast<const double2*>(r));
-        const double2 ob = __ldg(reinterpret_cast<const double2*>(r + M.split_plane));
-        const int4 tail = __ldg(r + 2 * M.split_plane);
-        const double thr = __hiloint2double(tail.y, tail.x);
-        const int an_a = (short)(tail.z & 0xffff), an_b = (short)(tail.z >> 16);
-        const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_a, oa.x, oa.y);
-        const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_b, ob.x, ob.y);
-        node = dsub(ia, ib) > thr ? 2 * node + 1 : 2 * node + 2;
+        SplitPlanes r[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) rec(node[q], kk[q], r[q]);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double thr = __hiloint2double(r[q].tail.y, r[q].tail.x);
+          const int an_a = (short)(r[q].tail.z & 0xffff), an_b = (short)(r[q].tail.z >> 16);
+          const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_a, r[q].oa.x, r[q].oa.y);
+          const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_b, r[q].ob.x, r[q].ob.y);
+          node[q] = dsub(ia, ib) > thr ? 2 * node[q] + 1 : 2 * node[q] + 2;
+        }
       }
-      sli[k] = (uint8_t)(node - S);
-      if (leaf_out) leaf_out[(long long)face * leaf_out_stride + (long long)t * K + k] = (uint8_t)(node - S);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        sli[kk[q]] = (uint8_t)(node[q] - S);
+        if (leaf_out) leaf_out[(long long)face * leaf_out_stride + (long long)t * K + kk[q]] = (uint8_t)(node[q] - S);
+      }
     }
     __syncthreads();
-    // (3) leaf sums in tree order, cur += shrinkage * delta (ert.cpp:118-126)
-    if (tid < L2) {
+#if BL_WD_CLOCK
+    long long c2 = clock64();
+#endif
+    // (3) leaf sums in tree order, cur += shrinkage * delta (ert.cpp:118-126): thread c < 2L
+    // adds coordinate c of the selected rows, kWdInFlight loads issued ahead of their adds.
+    // A level costs about K dependent fp64 adds here (the loads hide behind them: more in
+    // flight, or the coordinates split over a CTA cluster, measured no faster).
+    if (tid < L2 && !(BL_WD_PROBE & 1)) {
       double acc = 0.0;
       const double* lv = M.leaves + (long long)t * K * NL * L2 + tid;
       const int row = NL * L2;
       int k = 0;
-      for (; k + 32 <= K; k += 32) {
-        double v[32];
+      for (; k + kWdInFlight <= K; k += kWdInFlight) {
+        double v[kWdInFlight];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) v[u] = __ldg(lv + (long long)(k + u) * row + sli[k + u] * L2);
+        for (int u = 0; u < kWdInFlight; ++u) v[u] = __ldg(lv + (long long)(k + u) * row + sli[k + u] * L2);
 #pragma unroll
-        for (int u = 0; u < 32; ++u) acc = dadd(acc, v[u]);
+        for (int u = 0; u < kWdInFlight; ++u) acc = dadd(acc, v[u]);
       }
       for (; k < K; ++k) acc = dadd(acc, __ldg(lv + (long long)k * row + sli[k] * L2));
       sc[tid] = dadd(sc[tid], dmul(M.shrinkage, acc));  // the traversals' reads of sc are done
     }
     __syncthreads();
+#if BL_WD_CLOCK
+    long long c3 = clock64();
+    if (tid == 0) { clk[0] += c1 - c0; clk[1] += c2 - c1; clk[2] += c3 - c2; }
+#endif
   }
+#if BL_WD_CLOCK
+  if (tid == 0 && face == 0) printf("k_ert_wide face 0 cycles: xform %lld traverse %lld accum %lld\n", clk[0], clk[1], clk[2]);
+#endif
   // ert.cpp:132-133: box.x + p.x * box.w, box.y + p.y * box.h
   for (int c = tid; c < L2; c += blockDim.x)
     out_xy[(long long)face * L2 + c] = (c & 1) ? dadd((double)Y, dmul(sc[c], (double)H))
@@ -449,7 +511,7 @@ bool ert_wide_fits(const ErtDev& M) { return 2 * M.L <= kWdThreads && 2 * M.L <=
 void launch_ert_wide(const Launch& L, const ErtDev& M, const void* frames, int u8, int w, int h, long long pitch,
                      long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces,
                      int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err) {
-  const size_t smem = sizeof(double) * 2 * M.L + sizeof(double2) + (size_t)M.K;
+  const size_t smem = sizeof(double) * 4 * M.L + sizeof(double2) + (size_t)M.K;
   static size_t attr_u8 = 0, attr_f64 = 0;
   size_t& attr = u8 ? attr_u8 : attr_f64;
   if (smem > 48 * 1024 && smem > attr) {
