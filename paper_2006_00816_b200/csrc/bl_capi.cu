@@ -194,6 +194,9 @@ struct Slot {
   size_t h_stage_cap = 0;
   cudaEvent_t ev_h2d = nullptr, ev_done = nullptr, ev_meta = nullptr, ev_out = nullptr;
   cudaStream_t d2h = nullptr;  // this slot's result copies: never queued behind the other slot
+  // this slot's landmark cascade (lowest priority): overlaps the next batches' detection and,
+  // at small batches where one cascade fills few SMs, the other slots' cascades
+  cudaStream_t est = nullptr;
   bool busy = false;
   int n = 0, w = 0, h = 0, pix = 0, landmarks = 0;
   long long cap_faces = 0;
@@ -232,7 +235,6 @@ struct bl_ctx {
   int stage_launch[BL_STAGE_COUNT] = {};
   bool graphs = true;
   cudaStream_t hst = nullptr;  // H2D stream (input frames): never queued behind a D2H wait
-  cudaStream_t est = nullptr;  // ERT stream: batch i's cascade overlaps batch i+1's detection
   Slot slots[BL_MAX_IN_FLIGHT];
   uint64_t next_ticket = 1;
   int face_cap_per_frame = 64;  // device-side capacity of landmarked faces per frame
@@ -633,7 +635,7 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
   if (!same) {  // arenas may be reallocated: nothing may still be reading them
     CK(cudaStreamSynchronize(c->st));
     CK(cudaStreamSynchronize(c->hst));
-    CK(cudaStreamSynchronize(c->est));
+    for (Slot& o : c->slots) CK(cudaStreamSynchronize(o.est));
     CK(cudaStreamSynchronize(c->lane1));
     CK(cudaStreamSynchronize(c->user));
     for (Slot& o : c->slots) CK(cudaStreamSynchronize(o.d2h));
@@ -676,7 +678,7 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
     stage_mark(c, BL_STAGE_ERT);
     // the cascade only reads this slot's buffers and the frames, so (unless per-stage timing
     // wants one ordered stream) it runs on the ERT stream while the next batch detects
-    cudaStream_t es = c->timing ? c->st : c->est;
+    cudaStream_t es = c->timing ? c->st : S.est;
     if (es != c->st) {
       CK(cudaEventRecord(S.ev_det, c->st));
       CK(cudaStreamWaitEvent(es, S.ev_det, 0));
@@ -905,10 +907,10 @@ int bl_ctx_create(int device, bl_ctx** out) {
   c->device = device;
   CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->hst, cudaStreamNonBlocking));
-  {  // the cascade fills the gaps of the next batch's detection: lowest priority
+  {  // the cascades fill the gaps of the next batches' detection: lowest priority
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CK(cudaStreamCreateWithPriority(&c->est, cudaStreamNonBlocking, lo));
+    for (Slot& S : c->slots) CK(cudaStreamCreateWithPriority(&S.est, cudaStreamNonBlocking, lo));
   }
   c->st = c->user = c->own;
   CK(cudaStreamCreateWithFlags(&c->lane1, cudaStreamNonBlocking));
@@ -943,7 +945,6 @@ void bl_ctx_destroy(bl_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   if (c->hst) cudaStreamSynchronize(c->hst);
-  if (c->est) cudaStreamSynchronize(c->est);
   if (c->lane1) cudaStreamSynchronize(c->lane1);
   if (c->ev_lane) cudaEventDestroy(c->ev_lane);
   if (c->h_counts) cudaFreeHost(c->h_counts);
@@ -956,15 +957,18 @@ void bl_ctx_destroy(bl_ctx* c) {
       cudaStreamSynchronize(S.d2h);
       cudaStreamDestroy(S.d2h);
     }
+    if (S.est) {
+      cudaStreamSynchronize(S.est);
+      cudaStreamDestroy(S.est);
+    }
   }
-  cudaStream_t hst = c->hst, est = c->est, lane1 = c->lane1;
+  cudaStream_t hst = c->hst, lane1 = c->lane1;
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t own = c->own;
   delete c;  // DevBufs free on their device
   if (own) cudaStreamDestroy(own);
   if (hst) cudaStreamDestroy(hst);
-  if (est) cudaStreamDestroy(est);
   if (lane1) cudaStreamDestroy(lane1);
 }
 
@@ -980,7 +984,7 @@ int bl_ctx_synchronize(bl_ctx* c) {
   TRY(use_device(c));
   CK(cudaStreamSynchronize(c->st));
   CK(cudaStreamSynchronize(c->lane1));
-  CK(cudaStreamSynchronize(c->est));
+  for (Slot& S : c->slots) CK(cudaStreamSynchronize(S.est));
   CK(cudaStreamSynchronize(c->hst));
   return BL_OK;
 }
