@@ -147,7 +147,7 @@ int bl_detect_landmarks(bl_ctx* ctx, const void* frames, int pixel_type, int n, 
  * exactly like bl_detect / bl_detect_landmarks.  Up to BL_MAX_IN_FLIGHT batches may be in
  * flight, so later batches' H2D, the landmark cascade of an earlier one (its own stream) and
  * result copies overlap detection.  Tickets are collected in submission order. */
-#define BL_MAX_IN_FLIGHT 3
+#define BL_MAX_IN_FLIGHT 4
 int bl_submit(bl_ctx* ctx, const void* frames, int pixel_type, int n, int w, int h, size_t pitch,
               size_t frame_stride, int with_landmarks, uint64_t* ticket);
 int bl_collect(bl_ctx* ctx, uint64_t ticket, bl_detection* out, int64_t cap, int32_t* counts,

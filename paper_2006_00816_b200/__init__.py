@@ -56,7 +56,7 @@ assert DET_DTYPE.itemsize == 32
 BL_OK, BL_ERR_INVALID, BL_ERR_MODEL, BL_ERR_CUDA, BL_ERR_CAPACITY, BL_ERR_STATE, BL_ERR_IO = range(7)
 BL_PIX_U8, BL_PIX_F64 = 0, 1
 SCREEN_TCGEN05, SCREEN_FP32 = 0, 1
-MAX_IN_FLIGHT = 3  # BL_MAX_IN_FLIGHT
+MAX_IN_FLIGHT = 4  # BL_MAX_IN_FLIGHT
 STAGES = ["h2d", "pyramid", "gradhist", "features", "screen", "rescore", "nms", "ert", "d2h"]
 
 

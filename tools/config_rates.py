@@ -1,7 +1,7 @@
 """Throughput of the BASELINE.json configurations beyond the bench line (GPU box, 1 GPU).
 
 C2 320x240 x16, C3 1280x720 x64, C5 1920x1080 x256 (detect + 68 landmarks on every kept face,
-frames resident in HBM, 3 batches in flight through bl_submit / bl_collect) and C4 (landmarks
+frames resident in HBM, bl.MAX_IN_FLIGHT batches in flight through bl_submit / bl_collect) and C4 (landmarks
 only: 10k boxes through the 15x500xdepth-4 cascade).  The reference CPU path is timed beside
 each on a bounded sample with all host threads.  One JSON line per config on stdout:
     python tools/config_rates.py > profiles/r1v6_config_rates.jsonl"""

@@ -1,5 +1,5 @@
 """C2 (320x240 x16) latency breakdown on the GPU box: stage times, host cost of submit/collect,
-and throughput at 1..3 batches in flight."""
+and throughput at 1..4 batches in flight."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -28,7 +28,7 @@ for (w, h, b) in ((640, 480, 1), (320, 240, 16), (640, 480, 512)):
         torch.cuda.synchronize(); t2 = time.perf_counter(); ctx.collect(t, flat=True); t3 = time.perf_counter()
         ts.append(t1 - t0); tc.append(t3 - t2)
     print("  host submit ms", round(np.median(ts) * 1e3, 3), "collect (after sync) ms", round(np.median(tc) * 1e3, 3))
-    for inflight in (1, 2, 3):
+    for inflight in (1, 2, 3, 4):
         n = 60
         torch.cuda.synchronize(); t0 = time.perf_counter()
         pend = []
