@@ -8,11 +8,24 @@
 //
 // Roofline: HBM-bound.  Algorithmic bytes per output pixel: 8 B written + the source
 // level read once (1 B/px for u8 level 0, 8 B/px otherwise, 1.44 source px per output px).
+#include <stdint.h>
+
 #include "bl_internal.cuh"
 
 namespace blb {
 
-constexpr int kRsRows = 4;  // output rows per thread (column terms computed once)
+#ifndef BL_RS_ROWS
+#define BL_RS_ROWS 4
+#endif
+constexpr int kRsRows = BL_RS_ROWS;  // output rows per thread (column terms computed once)
+#ifndef BL_RS_PAIRS
+#define BL_RS_PAIRS 1
+#endif
+constexpr bool kRsPairs = BL_RS_PAIRS;  // k_resample2 where the destination allows
+#ifndef BL_RS_COLS
+#define BL_RS_COLS 2
+#endif
+constexpr int kRsCols = BL_RS_COLS;  // output columns per k_resample2 thread (2 or 4)
 
 template <typename Tin>
 __global__ void __launch_bounds__(256) k_resample(const Tin* __restrict__ src, int sw, int sh,
@@ -54,11 +67,80 @@ __global__ void __launch_bounds__(256) k_resample(const Tin* __restrict__ src, i
   }
 }
 
+// NC adjacent output columns per thread (16-B stores): the row terms computed once per NC
+// columns.  Needs 16-B aligned destination rows (the plan's arena).
+template <typename Tin, int NC>
+__global__ void __launch_bounds__(256) k_resample2(const Tin* __restrict__ src, int sw, int sh,
+                                                   long long s_pitch, long long s_fstride,
+                                                   double* __restrict__ dst, int dw, int dh, long long d_pitch,
+                                                   long long d_fstride, double rx, double ry) {
+  const int x = NC * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int y_first = (blockIdx.y * blockDim.y + threadIdx.y) * kRsRows;
+  if (x >= dw || y_first >= dh) return;
+  const Tin* s = src + (long long)blockIdx.z * s_fstride;
+  double* d = dst + (long long)blockIdx.z * d_fstride;
+  const double xmax = (double)(sw - 1);
+  int x0[NC], x1[NC];
+  double fx[NC], gx[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {  // image.cpp:145-149
+    double sx = dsub(dmul(dadd((double)(x + q), 0.5), rx), 0.5);
+    sx = sx < 0.0 ? 0.0 : (xmax < sx ? xmax : sx);
+    x0[q] = (int)sx;
+    x1[q] = min(x0[q] + 1, sw - 1);
+    fx[q] = dsub(sx, (double)x0[q]);
+    gx[q] = dsub(1.0, fx[q]);
+  }
+  const double ymax = (double)(sh - 1);
+#pragma unroll
+  for (int j = 0; j < kRsRows; ++j) {
+    const int y = y_first + j;
+    if (y >= dh) break;
+    double sy = dsub(dmul(dadd((double)y, 0.5), ry), 0.5);  // image.cpp:139-143
+    sy = sy < 0.0 ? 0.0 : (ymax < sy ? ymax : sy);
+    const int y0 = (int)sy;
+    const int y1 = min(y0 + 1, sh - 1);
+    const double fy = dsub(sy, (double)y0);
+    const double gy = dsub(1.0, fy);
+    const Tin* r0 = s + y0 * s_pitch;
+    const Tin* r1 = s + y1 * s_pitch;
+    double o[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {  // image.cpp:150-152
+      const double a = (double)__ldg(r0 + x0[q]), b = (double)__ldg(r0 + x1[q]);
+      const double c = (double)__ldg(r1 + x0[q]), e = (double)__ldg(r1 + x1[q]);
+      const double top = dadd(dmul(a, gx[q]), dmul(b, fx[q]));
+      const double bot = dadd(dmul(c, gx[q]), dmul(e, fx[q]));
+      o[q] = dadd(dmul(top, gy), dmul(bot, fy));
+    }
+    double* out = d + (long long)y * d_pitch + x;
+#pragma unroll
+    for (int q = 0; q < NC; q += 2) {
+      if (x + q + 1 < dw)
+        *reinterpret_cast<double2*>(out + q) = make_double2(o[q], o[q + 1]);
+      else if (x + q < dw)
+        out[q] = o[q];
+    }
+  }
+}
+
 void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
                      long long s_fstride, double* dst, int dw, int dh, long long d_pitch, long long d_fstride,
                      int n) {
   const double rx = double(sw) / dw, ry = double(sh) / dh;  // image.cpp:136-137
   const dim3 block(32, 8);
+  const bool vec = ((uintptr_t)dst & 15) == 0 && d_pitch % 2 == 0 && d_fstride % 2 == 0;
+  if (vec && kRsPairs) {
+    const dim3 grid2((unsigned)div_up(dw, 32 * kRsCols), (unsigned)div_up(dh, 8 * kRsRows), (unsigned)n);
+    if (src_u8)
+      k_resample2<uint8_t, kRsCols><<<grid2, block, 0, L.st>>>((const uint8_t*)src, sw, sh, s_pitch, s_fstride, dst, dw, dh,
+                                                       d_pitch, d_fstride, rx, ry);
+    else
+      k_resample2<double, kRsCols><<<grid2, block, 0, L.st>>>((const double*)src, sw, sh, s_pitch, s_fstride, dst, dw, dh,
+                                                      d_pitch, d_fstride, rx, ry);
+    ++*L.counter;
+    return;
+  }
   const dim3 grid((unsigned)div_up(dw, 32), (unsigned)div_up(dh, 8 * kRsRows), (unsigned)n);
   if (src_u8)
     k_resample<uint8_t><<<grid, block, 0, L.st>>>((const uint8_t*)src, sw, sh, s_pitch, s_fstride, dst, dw, dh,
