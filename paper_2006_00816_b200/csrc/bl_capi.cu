@@ -181,9 +181,9 @@ struct ErtWork {
   DevBuf cur, tf, leafs;
 };
 
-// One in-flight batch: its staged input, its device results and pinned host mirrors.  Three
-// slots let batch i+2's H2D, batch i+1's detection, and batch i's landmark cascade and
-// result copies overlap (bl_submit/collect).
+// One in-flight batch: its staged input, its device results and pinned host mirrors.
+// BL_MAX_IN_FLIGHT slots let later batches' H2D and detection overlap an earlier batch's
+// landmark cascade and result copies (bl_submit/collect).
 struct Slot {
   DevBuf input, flat, face_frame, meta, ert_out;
   ErtWork ert;                  // the slot's cascade runs on the ERT stream, beside the next detect
@@ -546,20 +546,25 @@ int check_frames(const void* frames, int pix, int n, int w, int h, size_t pitch,
 constexpr long long kErtWideMaxFaces = 400;  // measured crossover 300-600 faces (tools/diag_ert_wide.py)
 constexpr long long kErtFacesPerFrameGuess = 4;
 
+int ert_work_ensure(const ErtState& E, ErtWork& wk, int nf, bool leaf_scratch) {
+  TRY(wk.cur.ensure(sizeof(double) * 2 * E.dev.L * std::max(1, nf)));
+  TRY(wk.tf.ensure(sizeof(double2) * std::max(1, nf)));
+  if (leaf_scratch) TRY(wk.leafs.ensure((size_t)std::max(1, nf) * div_up(E.dev.K, 16) * 16 + 16));
+  return BL_OK;
+}
+
 int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix, int w, int h, long long pitch,
             long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces_dev,
             int nf, uint8_t* leaf_dev, double* out_xy, int* err_dev, long long expect_faces) {
   ErtState& E = c->ert;
   const Launch L{st, &c->launches};
   const int L2 = 2 * E.dev.L;
-  TRY(wk.cur.ensure(sizeof(double) * L2 * std::max(1, nf)));
-  TRY(wk.tf.ensure(sizeof(double2) * std::max(1, nf)));
+  TRY(ert_work_ensure(E, wk, nf, leaf_dev == nullptr));
   // leaf indices: the caller's [face][T*K] buffer, else a per-level scratch [face][K]
   long long leaf_stride = (long long)E.dev.T * E.dev.K;
   uint8_t* leaf = leaf_dev;
   if (!leaf) {
     leaf_stride = div_up(E.dev.K, 16) * 16;  // 16-B aligned rows: 128-bit index loads
-    TRY(wk.leafs.ensure((size_t)std::max(1, nf) * leaf_stride + 16));
     leaf = wk.leafs.as<uint8_t>();
   }
   CK(cudaMemsetAsync(err_dev, 0, sizeof(int), st));
@@ -644,6 +649,20 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
   const void* dev = nullptr;
   long long dp = 0, df = 0;
   const size_t es = pix == BL_PIX_U8 ? 1 : 8;
+  const long long cap_faces = std::max<long long>(1, (long long)n * c->face_cap_per_frame);
+  // Every slot is sized together on first use (and on growth), so a pipeline's later slots
+  // never allocate -- a synchronising cudaMalloc -- while earlier batches are in flight.
+  for (Slot& o : c->slots) {
+    if (!is_device_ptr(frames)) TRY(o.input.ensure(es * (size_t)n * w * h));
+    TRY(o.flat.ensure(sizeof(DevDet) * cap_faces));
+    TRY(o.face_frame.ensure(sizeof(int) * cap_faces));
+    TRY(o.meta.ensure(sizeof(int) * (n + 4)));
+    TRY(ensure_pinned(reinterpret_cast<void*&>(o.h_meta), o.h_meta_cap, sizeof(int) * (n + 4)));
+    if (landmarks) {
+      TRY(o.ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * cap_faces));
+      TRY(ert_work_ensure(c->ert, o.ert, (int)cap_faces, true));
+    }
+  }
   if (is_device_ptr(frames)) {
     dev = frames;
     dp = (long long)pitch;
@@ -666,7 +685,6 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
     df = (long long)w * h;
   }
   TRY(run_detect(c, dev, pix, n, w, h, dp, df, nullptr));
-  const long long cap_faces = std::max<long long>(1, (long long)n * c->face_cap_per_frame);
   TRY(S.flat.ensure(sizeof(DevDet) * cap_faces));
   TRY(S.face_frame.ensure(sizeof(int) * cap_faces));
   TRY(S.meta.ensure(sizeof(int) * (n + 4)));
@@ -741,7 +759,9 @@ int collect(bl_ctx* c, int s, bl_detection* out, int64_t cap, int32_t* counts, i
   const size_t bl = S.landmarks && landmarks ? sizeof(double) * 2 * c->ert.dev.L * tot : 0;
   const bool direct_d = !out || is_pinned_or_device(out);
   const bool direct_l = !bl || is_pinned_or_device(landmarks);
-  TRY(ensure_pinned(S.h_stage, S.h_stage_cap, (direct_d ? 0 : bd) + (direct_l ? 0 : bl) + 64));
+  const size_t need = (direct_d ? 0 : bd) + (direct_l ? 0 : bl) + 64;
+  if (S.h_stage_cap < need)  // grow every slot's staging at once (no host allocations mid-pipeline)
+    for (Slot& o : c->slots) TRY(ensure_pinned(o.h_stage, o.h_stage_cap, need + need / 2));
   char* stage = static_cast<char*>(S.h_stage);
   if (tot > 0 && out)
     CK(cudaMemcpyAsync(direct_d ? (void*)out : stage, S.flat.p, bd, cudaMemcpyDefault, S.d2h));

@@ -23,7 +23,7 @@ import paper_2006_00816_b200 as bl  # noqa: E402
 from paper_2006_00816_b200.synthetic import ring_frames_np  # noqa: E402
 
 
-def device_rate(ctx, frames, steps=10, warmup=3):
+def device_rate(ctx, frames, steps=40, warmup=4):
     dev = torch.from_numpy(frames).cuda()
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
