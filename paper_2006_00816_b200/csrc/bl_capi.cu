@@ -205,6 +205,14 @@ struct Slot {
 
 }  // namespace
 
+// Detection lanes (plan arenas + compute stream): consecutive in-flight batches rotate over
+// them so their detection stages overlap.  Two lanes saturate the GPU at large batches (the
+// bench's 512 frames: 3-4 lanes measured 1-3% slower); small, latency-bound batches (up to
+// kSmallBatchPx pixels, e.g. the 16-frame camera stream) rotate over all four.
+constexpr int kLanes = 4;
+constexpr int kLanesLarge = 2;
+constexpr long long kSmallBatchPx = 16LL << 20;
+
 struct bl_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
@@ -213,12 +221,12 @@ struct bl_ctx {
   uint64_t launches = 0;
   DetectorState det;
   ErtState ert;
-  // Two detection lanes (plan arenas + compute stream): consecutive in-flight batches
-  // alternate lanes, so batch i+1's pyramid / gradHist overlap batch i's later stages.
+  // Detection lanes (plan arenas + compute stream, see kLanes): consecutive in-flight batches
+  // rotate over them, so batch i+1's pyramid / gradHist overlap batch i's later stages.
   // Lane 0 runs on the caller's stream (c->user); `plan` / `st` point at the active lane.
-  Plan plans[2];
+  Plan plans[kLanes];
   Plan* plan = &plans[0];
-  cudaStream_t lane1 = nullptr;
+  cudaStream_t lanes[kLanes] = {};  // lanes[0] unused: lane 0 runs on `user`
   cudaStream_t user = nullptr;
   cudaEvent_t ev_lane = nullptr;
   // ERT working set
@@ -641,7 +649,7 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
     CK(cudaStreamSynchronize(c->st));
     CK(cudaStreamSynchronize(c->hst));
     for (Slot& o : c->slots) CK(cudaStreamSynchronize(o.est));
-    CK(cudaStreamSynchronize(c->lane1));
+    for (int l = 1; l < kLanes; ++l) CK(cudaStreamSynchronize(c->lanes[l]));
     CK(cudaStreamSynchronize(c->user));
     for (Slot& o : c->slots) CK(cudaStreamSynchronize(o.d2h));
   }
@@ -933,7 +941,7 @@ int bl_ctx_create(int device, bl_ctx** out) {
     for (Slot& S : c->slots) CK(cudaStreamCreateWithPriority(&S.est, cudaStreamNonBlocking, lo));
   }
   c->st = c->user = c->own;
-  CK(cudaStreamCreateWithFlags(&c->lane1, cudaStreamNonBlocking));
+  for (int l = 1; l < kLanes; ++l) CK(cudaStreamCreateWithFlags(&c->lanes[l], cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_lane, cudaEventDisableTiming));
   for (Slot& S : c->slots) {
     CK(cudaStreamCreateWithFlags(&S.d2h, cudaStreamNonBlocking));
@@ -965,7 +973,8 @@ void bl_ctx_destroy(bl_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   if (c->hst) cudaStreamSynchronize(c->hst);
-  if (c->lane1) cudaStreamSynchronize(c->lane1);
+  for (int l = 1; l < kLanes; ++l)
+    if (c->lanes[l]) cudaStreamSynchronize(c->lanes[l]);
   if (c->ev_lane) cudaEventDestroy(c->ev_lane);
   if (c->h_counts) cudaFreeHost(c->h_counts);
   for (Slot& S : c->slots) {
@@ -982,14 +991,17 @@ void bl_ctx_destroy(bl_ctx* c) {
       cudaStreamDestroy(S.est);
     }
   }
-  cudaStream_t hst = c->hst, lane1 = c->lane1;
+  cudaStream_t hst = c->hst;
+  cudaStream_t lanes[kLanes];
+  for (int l = 0; l < kLanes; ++l) lanes[l] = c->lanes[l];
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t own = c->own;
   delete c;  // DevBufs free on their device
   if (own) cudaStreamDestroy(own);
   if (hst) cudaStreamDestroy(hst);
-  if (lane1) cudaStreamDestroy(lane1);
+  for (int l = 1; l < kLanes; ++l)
+    if (lanes[l]) cudaStreamDestroy(lanes[l]);
 }
 
 int bl_ctx_set_stream(bl_ctx* c, void* stream) {
@@ -1003,7 +1015,7 @@ int bl_ctx_synchronize(bl_ctx* c) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
   TRY(use_device(c));
   CK(cudaStreamSynchronize(c->st));
-  CK(cudaStreamSynchronize(c->lane1));
+  for (int l = 1; l < kLanes; ++l) CK(cudaStreamSynchronize(c->lanes[l]));
   for (Slot& S : c->slots) CK(cudaStreamSynchronize(S.est));
   CK(cudaStreamSynchronize(c->hst));
   return BL_OK;
@@ -1140,8 +1152,7 @@ int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, d
   CK(cudaMemcpy(D.w32.p, w32.data(), sizeof(float) * w32.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(D.bias64.p, biases, sizeof(double) * kFilters, cudaMemcpyDefault));
   CK(cudaMemcpy(D.cut32.p, D.cut, sizeof(float) * kFilters, cudaMemcpyHostToDevice));
-  c->plans[0].valid = false;
-  c->plans[1].valid = false;
+  for (Plan& p : c->plans) p.valid = false;
   D.ready = true;
   return BL_OK;
 }
@@ -1258,13 +1269,14 @@ int bl_submit(bl_ctx* c, const void* frames, int pixel_type, int n, int w, int h
   const int s = (int)(t % BL_MAX_IN_FLIGHT);
   if (c->slots[s].busy)
     return set_err(BL_ERR_STATE, "%d batches in flight: collect one before submitting", BL_MAX_IN_FLIGHT);
-  const int lane = c->timing ? 0 : (int)(t & 1);
-  if (lane == 1) {  // after whatever the caller queued on its stream (e.g. device-resident inputs)
+  const int n_lanes = (long long)n * w * h <= kSmallBatchPx ? kLanes : kLanesLarge;
+  const int lane = c->timing ? 0 : (int)(t % n_lanes);
+  if (lane > 0) {  // after whatever the caller queued on its stream (e.g. device-resident inputs)
     CK(cudaEventRecord(c->ev_lane, c->user));
-    CK(cudaStreamWaitEvent(c->lane1, c->ev_lane, 0));
+    CK(cudaStreamWaitEvent(c->lanes[lane], c->ev_lane, 0));
   }
   c->plan = &c->plans[lane];
-  c->st = lane ? c->lane1 : c->user;
+  c->st = lane ? c->lanes[lane] : c->user;
   const int rc = enqueue(c, s, frames, pixel_type, n, w, h, pitch, frame_stride, with_landmarks != 0);
   c->plan = &c->plans[0];
   c->st = c->user;
