@@ -248,6 +248,22 @@ def test_nms_edge_cases(ctx, oracle):
     assert np.array_equal(ctx.nms(big), oracle.nms(big))
 
 
+@pytest.mark.parametrize("n,xmax,scale_max", [(1500, 600, 9), (2048, 3000, 16), (700, 6000, 9), (300, 500, 20)])
+def test_nms_compact_keys_and_fallback(ctx, oracle, n, xmax, scale_max):
+    """Up to 2048 detections sort as 16-B keys in shared memory (x, y < 4096, scale < 16,
+    rotation < 8 packed into 31 bits); frames outside those limits take the 32-B global-memory
+    path.  Both keep the reference's total order under heavy score / position ties."""
+    import paper_2006_00816_b200 as bl
+    r = rng(n + xmax)
+    d = np.zeros(n, bl.DET_DTYPE)
+    d["x"], d["y"] = r.integers(0, xmax, n), r.integers(0, 400, n)
+    d["x"][: n // 4] = d["x"][n // 4: 2 * (n // 4)]  # equal positions, different scale/rotation
+    d["w"] = d["h"] = r.integers(20, 200, n)
+    d["score"] = np.round(r.uniform(0, 1, n), 2)
+    d["scale_index"], d["rotation_index"] = r.integers(0, scale_max, n), r.integers(0, 5, n)
+    assert np.array_equal(ctx.nms(d), oracle.nms(d))
+
+
 # ---------------------------------------------------------------- detect_faces ----
 @pytest.mark.parametrize("case", ["c1", "planted", "qvga", "blank", "small"])
 def test_detect_golden(ctx, pattern_model, case):
