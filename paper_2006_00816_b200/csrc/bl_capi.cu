@@ -234,9 +234,6 @@ struct bl_ctx {
   DevBuf ert_out, ert_leaf, ert_boxes, ert_frames, ert_nfaces, ert_err, ert_input;
   // scratch for stage functions
   DevBuf s_a, s_b, s_c, s_d, s_e, s_desc;
-  // pinned host staging for counts
-  int* h_counts = nullptr;
-  size_t h_counts_cap = 0;
   bool timing = false;
   cudaEvent_t ev[BL_STAGE_COUNT + 1] = {};
   float stage_ms[BL_STAGE_COUNT] = {};
@@ -434,16 +431,15 @@ void stage_mark(bl_ctx* c, int stage) {
 }
 
 // ------------------------------------------------------------------ detection ----
-// Runs detect on n frames already resident on the device (`in`, element pitch/stride).
-// Leaves kept detections in P.flat (frame order) and P.n_faces on the device; copies the
-// per-frame counts to h_counts (synchronising).
+// Enqueues detect on n frames already resident on the device (`in`, element pitch/stride) on
+// the active lane's stream: leaves each frame's kept detections in P.kept / P.kept_count on
+// the device (no host synchronisation).
 int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long long pitch,
                long long fstride, int64_t* total_out) {
   Plan& P = *c->plan;
   TRY(build_plan(c, P, n, w, h, pix));
   const Launch L = launch_of(c);
   const DetectorState& D = c->det;
-  uint64_t l0 = c->launches;
 
   // level 0 descriptor points at the caller's frames
   if (!P.scored.empty() && P.scored[0] == 0) {
@@ -498,17 +494,7 @@ int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long lon
   stage_mark(c, BL_STAGE_NMS);
   launch_nms(L, P.dets.as<DevDet>(), P.det_count.as<int>(), P.cap_pf, n, 0.5, P.kept.as<DevDet>(),
              P.kept_count.as<int>(), P.gkeys.p, P.gkeys_pf);
-  (void)l0;
   (void)total_out;
-  return BL_OK;
-}
-
-int ensure_counts(bl_ctx* c, size_t n) {
-  if (c->h_counts_cap >= n) return BL_OK;
-  if (c->h_counts) cudaFreeHost(c->h_counts);
-  c->h_counts = nullptr;
-  CK(cudaMallocHost(&c->h_counts, sizeof(int) * (n + 2)));
-  c->h_counts_cap = n;
   return BL_OK;
 }
 
@@ -976,7 +962,6 @@ void bl_ctx_destroy(bl_ctx* c) {
   for (int l = 1; l < kLanes; ++l)
     if (c->lanes[l]) cudaStreamSynchronize(c->lanes[l]);
   if (c->ev_lane) cudaEventDestroy(c->ev_lane);
-  if (c->h_counts) cudaFreeHost(c->h_counts);
   for (Slot& S : c->slots) {
     if (S.h_meta) cudaFreeHost(S.h_meta);
     if (S.h_stage) cudaFreeHost(S.h_stage);
