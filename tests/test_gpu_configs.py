@@ -86,3 +86,19 @@ def test_c5_1080p_batch(ctx, oracle, pattern_model):
     again = ctx.detect_landmarks(frames)
     for k in range(32):
         assert np.array_equal(again[0][k], dets[k]) and np.array_equal(again[1][k], lms[k])
+
+
+def test_bench_batch_vs_small_batch_kernels(ctx, pattern_model):
+    """The bench's 512-frame batch runs 24-row gradHist segments and the 4-faces-per-CTA
+    cascade; a 3-frame batch of the same frames runs 1-row segments and the face-per-CTA
+    cascade (k_ert_wide).  Both configurations give bit-identical detections and landmarks."""
+    frames = ring_frames_np(512, 640, 480, seed=606)
+    ert = random_ert(T=3, K=120, F=4, seed=61)
+    ctx.upload_detector(pattern_model)
+    ctx.upload_ert(ert)
+    dets, lms = ctx.detect_landmarks(frames)
+    assert sum(len(d) for d in dets) > 512
+    for lo in (0, 200, 509):
+        d3, l3 = ctx.detect_landmarks(frames[lo:lo + 3])
+        for k in range(3):
+            assert np.array_equal(d3[k], dets[lo + k]) and np.array_equal(l3[k], lms[lo + k])
