@@ -247,6 +247,7 @@ struct bl_ctx {
   // landmark cascade kernel: auto (k_ert_wide for small batches, else k_ert_cascade), or forced
   // by BL_ERT=wide|cascade|levels (experiments)
   int ert_mode = 0;
+  bool pyr_fuse = true;  // fused resample pairs over unscored levels (BL_PYR_FUSE=0 disables)
 };
 
 namespace {
@@ -452,12 +453,24 @@ int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long lon
     }
   }
   stage_mark(c, BL_STAGE_PYRAMID);
-  // pyramid chain (image.cpp:162-170): level k from level k-1, every frame at once
+  // pyramid chain (image.cpp:162-170): level k from level k-1, every frame at once.  A level
+  // no window scores (below the smallest eligible face) is read only by the next step, so
+  // the two steps run fused (k_resample_pair) and that level never reaches HBM.
+  std::vector<char> is_scored(P.n_levels + 1, 0);
+  for (int k : P.scored) is_scored[k] = 1;
   for (int k = 1; k < P.n_levels; ++k) {
     const void* src = k == 1 ? in : (const void*)(P.arena.as<double>() + P.arena_off[k - 1]);
     const int src_u8 = (k == 1 && pix == BL_PIX_U8);
     const long long sp = k == 1 ? pitch : P.lpitch[k - 1];
     const long long sf = k == 1 ? fstride : (long long)P.lpitch[k - 1] * P.lh[k - 1];
+    if (c->pyr_fuse && !is_scored[k] && k + 1 < P.n_levels &&
+        resample_pair_fits(P.lw[k - 1], P.lh[k - 1], P.lw[k], P.lh[k], P.lw[k + 1], P.lh[k + 1])) {
+      launch_resample_pair(L, src, src_u8, P.lw[k - 1], P.lh[k - 1], sp, sf, P.lw[k], P.lh[k],
+                           P.arena.as<double>() + P.arena_off[k + 1], P.lw[k + 1], P.lh[k + 1], P.lpitch[k + 1],
+                           (long long)P.lpitch[k + 1] * P.lh[k + 1], n);
+      ++k;
+      continue;
+    }
     launch_resample(L, src, src_u8, P.lw[k - 1], P.lh[k - 1], sp, sf, P.arena.as<double>() + P.arena_off[k],
                     P.lw[k], P.lh[k], P.lpitch[k], (long long)P.lpitch[k] * P.lh[k], n);
   }
@@ -947,6 +960,7 @@ int bl_ctx_create(int device, bl_ctx** out) {
   }
   set_direction_table(ux, uy);
   if (const char* e = std::getenv("BL_SCREEN")) c->screen = std::strcmp(e, "fp32") == 0 ? BL_SCREEN_FP32 : BL_SCREEN_TCGEN05;
+  if (const char* e = std::getenv("BL_PYR_FUSE")) c->pyr_fuse = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT"))
     c->ert_mode = !std::strcmp(e, "cascade") ? 1 : !std::strcmp(e, "wide") ? 2 : !std::strcmp(e, "levels") ? 3 : 0;
   CK(cudaGetLastError());

@@ -183,6 +183,10 @@ struct Launch {
 // bl_pyramid.cu
 void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
                      long long s_fstride, double* dst, int dw, int dh, long long d_pitch, long long d_fstride, int n);
+bool resample_pair_fits(int sw, int sh, int mw, int mh, int dw, int dh);
+void launch_resample_pair(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
+                          long long s_fstride, int mw, int mh, double* dst, int dw, int dh, long long d_pitch,
+                          long long d_fstride, int n);
 // bl_hog.cu
 void set_direction_table(const double* ux, const double* uy);
 void launch_grad(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, int s_lo, int s_hi, const void* base,

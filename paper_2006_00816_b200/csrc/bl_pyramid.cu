@@ -124,6 +124,125 @@ __global__ void __launch_bounds__(256) k_resample2(const Tin* __restrict__ src, 
   }
 }
 
+// Two chained steps in one pass, for a level nobody but the next step reads (a level below
+// the smallest eligible face size: C5 levels 1-5, C3 1-3): each CTA computes the
+// region of the intermediate level m its output tile needs into shared memory (from level
+// k-1, the same arithmetic as k_resample, so every value is bit-identical wherever it is
+// computed -- ~14% of them twice at tile borders), then the tile of level k+1 from it.  Level
+// m never reaches HBM: its write and re-read (the bulk of the pyramid's bytes at 1080p) go.
+constexpr int kPrTX = 64, kPrTY = 32;  // output tile of level k+1
+
+BL_DEV void resample_coord(int x, double r, int n_src, int& x0, int& x1, double& f) {  // image.cpp:139-149
+  double sx = dsub(dmul(dadd((double)x, 0.5), r), 0.5);
+  const double xmax = (double)(n_src - 1);
+  sx = sx < 0.0 ? 0.0 : (xmax < sx ? xmax : sx);
+  x0 = (int)sx;
+  x1 = min(x0 + 1, n_src - 1);
+  f = dsub(sx, (double)x0);
+}
+
+BL_DEV double bilerp(double a, double b, double c, double e, double fx, double fy) {  // image.cpp:150-152
+  const double top = dadd(dmul(a, dsub(1.0, fx)), dmul(b, fx));
+  const double bot = dadd(dmul(c, dsub(1.0, fx)), dmul(e, fx));
+  return dadd(dmul(top, dsub(1.0, fy)), dmul(bot, fy));
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(256) k_resample_pair(const Tin* __restrict__ src, int sw, int sh, long long s_pitch,
+                                                       long long s_fstride, int mw, int mh, double rx1, double ry1,
+                                                       double* __restrict__ dst, int dw, int dh, long long d_pitch,
+                                                       long long d_fstride, double rx2, double ry2) {
+  extern __shared__ double mid[];
+  const int X0 = blockIdx.x * kPrTX, Y0 = blockIdx.y * kPrTY;
+  const int X1 = min(X0 + kPrTX, dw) - 1, Y1 = min(Y0 + kPrTY, dh) - 1;
+  const Tin* s = src + (long long)blockIdx.z * s_fstride;
+  double* d = dst + (long long)blockIdx.z * d_fstride;
+  // the intermediate region [mx_lo, mx_hi] x [my_lo, my_hi] the tile's taps touch (x0 and x1
+  // are non-decreasing in the output coordinate)
+  int mx_lo, mx_hi, my_lo, my_hi, t0;
+  double tf;
+  resample_coord(X0, rx2, mw, mx_lo, t0, tf);
+  resample_coord(X1, rx2, mw, t0, mx_hi, tf);
+  resample_coord(Y0, ry2, mh, my_lo, t0, tf);
+  resample_coord(Y1, ry2, mh, t0, my_hi, tf);
+  const int RW = mx_hi - mx_lo + 1, RH = my_hi - my_lo + 1;
+  // 32 x 8 threads: a thread owns columns tx, tx + 32, ... and rows ty, ty + 8, ... of each
+  // phase, so its column terms are computed once per column, its row terms once per row
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  constexpr int kCols1 = 4;  // region columns per thread (RW <= 128 for rx < 2)
+  int cx0[kCols1], cx1[kCols1];
+  double cfx[kCols1];
+#pragma unroll
+  for (int q = 0; q < kCols1; ++q) resample_coord(min(mx_lo + tx + 32 * q, mx_hi), rx1, sw, cx0[q], cx1[q], cfx[q]);
+  for (int r = ty; r < RH; r += 8) {
+    int y0, y1;
+    double fy;
+    resample_coord(my_lo + r, ry1, sh, y0, y1, fy);
+    const Tin* r0 = s + y0 * s_pitch;
+    const Tin* r1 = s + y1 * s_pitch;
+#pragma unroll
+    for (int q = 0; q < kCols1; ++q) {
+      const int c = tx + 32 * q;
+      if (c < RW)
+        mid[r * RW + c] = bilerp((double)__ldg(r0 + cx0[q]), (double)__ldg(r0 + cx1[q]), (double)__ldg(r1 + cx0[q]),
+                                 (double)__ldg(r1 + cx1[q]), cfx[q], fy);
+    }
+  }
+  __syncthreads();
+  const int TW = X1 - X0 + 1, TH = Y1 - Y0 + 1;
+  constexpr int kCols2 = kPrTX / 32;
+  int ox0[kCols2], ox1[kCols2];
+  double ofx[kCols2];
+#pragma unroll
+  for (int q = 0; q < kCols2; ++q) {
+    resample_coord(X0 + min(tx + 32 * q, TW - 1), rx2, mw, ox0[q], ox1[q], ofx[q]);
+    ox0[q] -= mx_lo;
+    ox1[q] -= mx_lo;
+  }
+  for (int r = ty; r < TH; r += 8) {
+    int y0, y1;
+    double fy;
+    resample_coord(Y0 + r, ry2, mh, y0, y1, fy);
+    const double* m0 = mid + (y0 - my_lo) * RW;
+    const double* m1 = mid + (y1 - my_lo) * RW;
+    double* out = d + (long long)(Y0 + r) * d_pitch + X0;
+#pragma unroll
+    for (int q = 0; q < kCols2; ++q) {
+      const int c = tx + 32 * q;
+      if (c < TW) out[c] = bilerp(m0[ox0[q]], m0[ox1[q]], m1[ox0[q]], m1[ox1[q]], ofx[q], fy);
+    }
+  }
+}
+
+bool resample_pair_fits(int sw, int sh, int mw, int mh, int dw, int dh) {
+  // ratios < 1.9: a tile's region stays within 4 x 32 columns (floor(63 * r) + 4 <= 123)
+  return 10LL * sw < 19LL * mw && 10LL * sh < 19LL * mh && 10LL * mw < 19LL * dw && 10LL * mh < 19LL * dh;
+}
+
+void launch_resample_pair(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
+                          long long s_fstride, int mw, int mh, double* dst, int dw, int dh, long long d_pitch,
+                          long long d_fstride, int n) {
+  const double rx1 = double(sw) / mw, ry1 = double(sh) / mh;  // image.cpp:136-137, each step
+  const double rx2 = double(mw) / dw, ry2 = double(mh) / dh;
+  const dim3 grid((unsigned)div_up(dw, kPrTX), (unsigned)div_up(dh, kPrTY), (unsigned)n);
+  // region bound: floor((T - 1) * r) + 3 taps, +1 for the rounding of the computed coordinate
+  const int rw = (int)((kPrTX - 1) * rx2) + 4, rh = (int)((kPrTY - 1) * ry2) + 4;
+  const size_t smem = sizeof(double) * rw * rh;
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_resample_pair<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_resample_pair<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  if (src_u8)
+    k_resample_pair<uint8_t><<<grid, 256, smem, L.st>>>((const uint8_t*)src, sw, sh, s_pitch, s_fstride, mw, mh, rx1,
+                                                        ry1, dst, dw, dh, d_pitch, d_fstride, rx2, ry2);
+  else
+    k_resample_pair<double><<<grid, 256, smem, L.st>>>((const double*)src, sw, sh, s_pitch, s_fstride, mw, mh, rx1,
+                                                       ry1, dst, dw, dh, d_pitch, d_fstride, rx2, ry2);
+  ++*L.counter;
+}
+
 void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
                      long long s_fstride, double* dst, int dw, int dh, long long d_pitch, long long d_fstride,
                      int n) {

@@ -102,3 +102,23 @@ def test_bench_batch_vs_small_batch_kernels(ctx, pattern_model):
         d3, l3 = ctx.detect_landmarks(frames[lo:lo + 3])
         for k in range(3):
             assert np.array_equal(d3[k], dets[lo + k]) and np.array_equal(l3[k], lms[lo + k])
+
+
+def test_fused_unscored_levels_bit_identical(monkeypatch, pattern_model):
+    """1080p: levels 1-5 lie below the smallest eligible face, so the chain runs them as fused
+    pairs (k_resample_pair: the unscored level stays in shared memory).  Detections and
+    landmarks equal those of the level-by-level chain (BL_PYR_FUSE=0) bit for bit."""
+    import paper_2006_00816_b200 as bl
+    frames = ring_frames_np(6, 1920, 1080, seed=707)
+    ert = random_ert(T=2, K=40, F=4, seed=71)
+    out = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("BL_PYR_FUSE", fuse)
+        c = bl.Context(0)
+        c.upload_detector(pattern_model)
+        c.upload_ert(ert)
+        out[fuse] = c.detect_landmarks(frames)
+        c.close()
+    assert sum(len(d) for d in out["1"][0]) > 0
+    for k in range(len(frames)):
+        assert np.array_equal(out["1"][0][k], out["0"][0][k]) and np.array_equal(out["1"][1][k], out["0"][1][k])

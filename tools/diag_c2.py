@@ -10,7 +10,7 @@ from paper_2006_00816_b200.synthetic import ring_frames_np
 
 det, ert = bench.load_models()
 ctx = bl.Context(0); ctx.upload_detector(det); ctx.upload_ert(ert)
-for (w, h, b) in ((640, 480, 1), (320, 240, 16), (640, 480, 512)):
+for (w, h, b) in [tuple(int(v) for v in a.split("x")) for a in sys.argv[1:]] or ((640, 480, 1), (320, 240, 16), (640, 480, 512)):
     frames = ring_frames_np(b, w, h, seed=77)
     dev = torch.from_numpy(frames).cuda()
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
