@@ -565,7 +565,6 @@ int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix
             int nf, uint8_t* leaf_dev, double* out_xy, int* err_dev, long long expect_faces) {
   ErtState& E = c->ert;
   const Launch L{st, &c->launches};
-  const int L2 = 2 * E.dev.L;
   TRY(ert_work_ensure(E, wk, nf, leaf_dev == nullptr));
   // leaf indices: the caller's [face][T*K] buffer, else a per-level scratch [face][K]
   long long leaf_stride = (long long)E.dev.T * E.dev.K;
