@@ -304,6 +304,10 @@ def run_ours(args):
                 "traffic_unit": "GB per step (ncu dram__bytes_read+write.sum, profiles/traffic.json)",
                 "peak_source": peak_note}
     roofline["kernel"] = dom
+    if dom == "gradhist":  # what actually bounds it (ncu, profiles/r1v6_ncu_kernels.txt, DESIGN §5/§9)
+        roofline["limiter"] = ("instruction issue: 62% issue-active at 16 warps/SM, ~108 instructions per level "
+                               "pixel for the exact fp64 gradient/orientation/histogram (fp64 pipe: frac_fp64 in "
+                               "stages_ms.gradhist)")
 
     # ---- CPU baseline (rank 0, N=1): the reference library on this box's cores
     cpu = None
