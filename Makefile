@@ -23,7 +23,7 @@ CPPLIB   := $(PKG)/libblinkline_gpu.so
 EXACT_CU := bl_pyramid bl_hog bl_exact bl_ert
 FAST_CU  := bl_classify bl_screen_tc bl_capi
 JSON_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
-HOST_CPP := bl_io bl_run
+HOST_CPP := bl_io bl_run bl_multi
 OBJS     := $(addprefix $(BUILD)/,$(addsuffix .o,$(EXACT_CU) $(FAST_CU) $(HOST_CPP)))
 HDRS     := $(CSRC)/bl_internal.cuh include/blinkline_b200.h
 
@@ -43,6 +43,9 @@ $(BUILD)/bl_io.o: $(CSRC)/bl_io.cpp include/blinkline_b200.h | $(BUILD)
 
 $(BUILD)/bl_run.o: $(CSRC)/bl_run.cpp include/blinkline_b200.h | $(BUILD)
 	$(CXX) -std=c++17 -O2 -fPIC -c $< -o $@
+
+$(BUILD)/bl_multi.o: $(CSRC)/bl_multi.cpp include/blinkline_b200.h | $(BUILD)
+	$(CXX) -std=c++17 -O2 -fPIC -Wall -c $< -o $@
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fPIC -lcudart_static -lrt -lpthread -ldl

@@ -155,6 +155,36 @@ int bl_collect(bl_ctx* ctx, uint64_t ticket, bl_detection* out, int64_t cap, int
 /* Device capacity of landmarked faces per frame for the landmark pipelines (default 64); the
  * synchronous calls grow it automatically, bl_collect reports BL_ERR_CAPACITY. */
 int bl_ctx_set_face_capacity(bl_ctx* ctx, int faces_per_frame);
+int bl_ctx_get_face_capacity(bl_ctx* ctx, int* faces_per_frame);
+
+/* ------------------------------------------------------------- multi-device ---- */
+/* Frame sharding over several GPUs in one process (replaces the reference's
+ * frame-parallel worker pool, pipeline.cpp:230-324, with one worker per device).  One context
+ * per listed device (a device may be listed more than once), each driven by its own host
+ * thread.  Frames are independent: a batch is split into contiguous per-device shards (sizes
+ * differ by at most one, lower slots take the extra frame), every device runs detect +
+ * landmarks on its shard through bl_submit/bl_collect with its own model replica, and the
+ * results are gathered in frame order.  No collective: the gather is on the host. */
+typedef struct bl_multi bl_multi;
+int bl_multi_create(const int* devices, int n_devices, bl_multi** out);
+void bl_multi_destroy(bl_multi* m);
+int bl_multi_size(bl_multi* m, int* n_devices);
+/* The context of device slot i (configuration, model files via bl_ert_file_upload). */
+int bl_multi_context(bl_multi* m, int i, bl_ctx** ctx);
+/* Frames per submitted batch = max(1, pixels_per_submit / (w*h)) (default 160 Mi pixels). */
+int bl_multi_set_batch_pixels(bl_multi* m, int64_t pixels_per_submit);
+/* Replicate a model to every device (arguments as bl_detector_upload / bl_ert_upload). */
+int bl_multi_detector_upload(bl_multi* m, const double* weights, const double* biases, double threshold,
+                             int window_cells, int cell_px, int scale_num, int scale_den,
+                             double min_face_ratio);
+int bl_multi_ert_upload(bl_multi* m, int L, int T, int K, int F, double shrinkage, const double* mean_xy,
+                        const int32_t* anchors, const double* split_params, const double* leaves);
+/* replaces: detect_frame + landmark_frame over a frame sequence (pipeline.cpp:159-190,
+ * 230-324).  Outputs exactly as bl_detect_landmarks (landmarks NULL = detection only).
+ * device_ms (optional, n_devices): wall time of each device's shard. */
+int bl_multi_detect_landmarks(bl_multi* m, const void* frames, int pixel_type, int n, int w, int h,
+                              size_t pitch, size_t frame_stride, bl_detection* out, int64_t cap,
+                              int32_t* counts, int64_t* total, double* landmarks, double* device_ms);
 
 /* ----------------------------------------------------------- stage functions ---- */
 /* Device implementations of the reference's stage API, for the drop-in C++ layer and the

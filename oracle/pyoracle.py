@@ -449,5 +449,16 @@ class Reference(_Base):
 
 
 # Synthetic-input generators live with the product (bench.py uses them without importing
-# oracle/); re-exported here for the tests.
-from paper_2006_00816_b200.synthetic import face68_mean_shape_np, random_ert, ring_frames_np  # noqa: E402,F401
+# oracle/); re-exported here for the tests.  Loaded by file path: importing the package would
+# map the GPU library into a CPU-checker process (the --impl reference arm must not).
+def _load_synthetic():
+    import importlib.util
+    path = os.path.join(os.path.dirname(HERE), "paper_2006_00816_b200", "synthetic.py")
+    spec = importlib.util.spec_from_file_location("_bl_synthetic", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+_syn = _load_synthetic()
+face68_mean_shape_np, random_ert, ring_frames_np = _syn.face68_mean_shape_np, _syn.random_ert, _syn.ring_frames_np

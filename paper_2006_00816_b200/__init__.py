@@ -29,7 +29,7 @@ import threading
 import numpy as np
 
 __all__ = [
-    "Context", "ModelError", "DET_DTYPE", "library_path", "lib",
+    "Context", "MultiContext", "ModelError", "DET_DTYPE", "library_path", "lib",
     "build_pyramid", "downscale_bilinear", "compute_gradients", "histogramize", "cell_energy",
     "compute_features", "extract_features", "score_separable", "score_dense", "nms",
     "orientation_bins", "detect_faces", "predict_landmarks", "default_context",
@@ -103,6 +103,16 @@ _SIGS = {
     "bl_submit": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _sz, _sz, C.c_int, _P(_u64)]),
     "bl_collect": (C.c_int, [_vp, _u64, _vp, _i64, _vp, _P(_i64), _vp]),
     "bl_ctx_set_face_capacity": (C.c_int, [_vp, C.c_int]),
+    "bl_ctx_get_face_capacity": (C.c_int, [_vp, _P(C.c_int)]),
+    "bl_multi_create": (C.c_int, [_vp, C.c_int, _P(_vp)]),
+    "bl_multi_destroy": (None, [_vp]),
+    "bl_multi_size": (C.c_int, [_vp, _P(C.c_int)]),
+    "bl_multi_context": (C.c_int, [_vp, C.c_int, _P(_vp)]),
+    "bl_multi_set_batch_pixels": (C.c_int, [_vp, _i64]),
+    "bl_multi_detector_upload": (C.c_int, [_vp, _vp, _vp, _dbl, C.c_int, C.c_int, C.c_int, C.c_int, _dbl]),
+    "bl_multi_ert_upload": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _dbl, _vp, _vp, _vp, _vp]),
+    "bl_multi_detect_landmarks": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _sz, _sz, _vp, _i64,
+                                            _vp, _P(_i64), _vp, _vp]),
     "bl_landmarks": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _sz, _sz, _vp, _vp, _i64, _vp, _vp]),
     "bl_detect_landmarks": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _sz, _sz, _vp, _i64, _vp,
                                       _P(_i64), _vp]),
@@ -345,13 +355,14 @@ class Context:
         a, pix, n, h, w = _frames(frames)
         t = C.c_uint64(0)
         _err(lib.bl_submit(self._h, _addr(a), pix, n, w, h, w, w * h, int(landmarks), C.byref(t)))
-        self._inflight[t.value] = (a, n, landmarks)  # keep the frames alive until collected
+        # keep the frames alive until collected; the batch's device face capacity is fixed at submit
+        self._inflight[t.value] = (a, n, landmarks, n * self.face_capacity())
         return t.value
 
     def collect(self, ticket, flat=True, cap=None):
         if ticket not in self._inflight:
             raise RuntimeError("blinkline_b200: unknown or collected ticket")
-        a, n, landmarks = self._inflight[ticket]
+        a, n, landmarks, dev_cap = self._inflight[ticket]
         cap = cap or max(1024, 64 * n)
         while True:
             out = np.empty(cap, DET_DTYPE)
@@ -360,8 +371,10 @@ class Context:
             total = C.c_int64(0)
             rc = lib.bl_collect(self._h, ticket, out.ctypes.data, cap, counts.ctypes.data, C.byref(total),
                                 lm.ctypes.data if lm is not None else None)
-            if rc == BL_ERR_CAPACITY and total.value > cap:
-                cap = int(total.value)  # results stay on the device; collect again
+            if rc == BL_ERR_CAPACITY and cap < total.value <= dev_cap:
+                # only the OUTPUT buffer was short: the results stay on the device, collect again
+                # (beyond the device face capacity the batch is gone: raise the real cause)
+                cap = int(total.value)
                 continue
             del self._inflight[ticket]
             _err(rc, total.value)
@@ -371,6 +384,11 @@ class Context:
 
     def set_face_capacity(self, faces_per_frame):
         _err(lib.bl_ctx_set_face_capacity(self._h, int(faces_per_frame)))
+
+    def face_capacity(self):
+        v = C.c_int(0)
+        _err(lib.bl_ctx_get_face_capacity(self._h, C.byref(v)))
+        return v.value
 
     def landmarks(self, frames, frame_of_box, boxes, want_leaves=False):
         """predict_landmarks for (frame, box) pairs -> (n_boxes, L, 2) [, leaf idx (n_boxes, T*K)]."""
@@ -517,6 +535,79 @@ def plan_geometry(w, h, window_cells=10, cell_px=8, scale_num=5, scale_den=6, mi
 
 # ------------------------------------------------ reference-named module functions
 _tls = threading.local()
+
+
+
+class MultiContext:
+    """Frame sharding over several GPUs in one process (bl_multi_*): one
+    context and one host worker thread per listed device, contiguous frame shards, results
+    gathered in frame order on the host.  ``devices`` may repeat a device."""
+
+    def __init__(self, devices):
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        _err(lib.bl_multi_create(devs, len(devices), C.byref(h)))
+        self._h = h
+        self.devices = list(devices)
+        self.ert_L = None
+        self.last_device_ms = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.bl_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_batch_pixels(self, pixels):
+        _err(lib.bl_multi_set_batch_pixels(self._h, int(pixels)))
+
+    def upload_detector(self, model):
+        w = _np(model["weights"], np.float64).reshape(5, 3100)
+        b = _np(model["biases"], np.float64).reshape(5)
+        _err(lib.bl_multi_detector_upload(self._h, w.ctypes.data, b.ctypes.data, float(model["threshold"]),
+                                          int(model.get("window_cells", 10)), int(model.get("cell_px", 8)),
+                                          int(model.get("scale_num", 5)), int(model.get("scale_den", 6)),
+                                          float(model.get("min_face_ratio", 0.2))))
+
+    def upload_ert(self, ert):
+        m = _np(ert["mean_xy"], np.float64)
+        a = _np(ert["anchors"], np.int32)
+        sp = _np(ert["split_params"], np.float64)
+        lv = _np(ert["leaves"], np.float64)
+        _err(lib.bl_multi_ert_upload(self._h, int(ert["L"]), int(ert["T"]), int(ert["K"]), int(ert["F"]),
+                                     float(ert["shrinkage"]), m.ctypes.data, a.ctypes.data, sp.ctypes.data,
+                                     lv.ctypes.data))
+        self.ert_L = int(ert["L"])
+
+    def detect_landmarks(self, frames, landmarks=True, flat=True):
+        """Host frames (n, h, w) u8/f64 -> (dets, counts, landmarks) back to back in frame order
+        (landmarks=False: (dets, counts))."""
+        a, pix, n, h, w = _frames(frames)
+        if hasattr(a, "is_cuda") and a.is_cuda:
+            raise ValueError("MultiContext takes host frames (each device uploads its own shard)")
+        cap = max(1, n * 64)
+        out = np.empty(cap, DET_DTYPE)
+        lm = np.empty((cap, self.ert_L or 1, 2)) if landmarks else None
+        counts = np.zeros(n, np.int32)
+        total = _i64()
+        ms = np.zeros(len(self.devices))
+        _err(lib.bl_multi_detect_landmarks(self._h, _addr(a), pix, n, w, h, w, w * h, out.ctypes.data, cap,
+                                           counts.ctypes.data, C.byref(total),
+                                           lm.ctypes.data if lm is not None else None, ms.ctypes.data))
+        self.last_device_ms = ms
+        t = int(total.value)
+        if flat:
+            return (out[:t], counts, lm[:t]) if landmarks else (out[:t], counts)
+        offs = np.concatenate([[0], np.cumsum(counts)])
+        dets = [out[offs[i]:offs[i + 1]] for i in range(n)]
+        if not landmarks:
+            return dets
+        return dets, [lm[:t][offs[i]:offs[i + 1]] for i in range(n)]
 
 
 def default_context(device: int | None = None) -> Context:

@@ -825,6 +825,21 @@ int detect_common(bl_ctx* c, const void* frames, int pix, int n, int w, int h, s
   return BL_OK;
 }
 
+// Model uploads overwrite device buffers that in-flight batches read: refuse while a submitted
+// batch is uncollected, and drain every context stream before the first write.
+int quiesce_for_upload(bl_ctx* c) {
+  for (const Slot& S : c->slots)
+    if (S.busy) return set_err(BL_ERR_STATE, "collect the submitted batches before uploading a model");
+  CK(cudaStreamSynchronize(c->user));
+  CK(cudaStreamSynchronize(c->hst));
+  for (int l = 1; l < kLanes; ++l) CK(cudaStreamSynchronize(c->lanes[l]));
+  for (const Slot& S : c->slots) {
+    CK(cudaStreamSynchronize(S.est));
+    CK(cudaStreamSynchronize(S.d2h));
+  }
+  return BL_OK;
+}
+
 // Copies `bytes` from a user pointer (host or device) into scratch, returns a device pointer.
 int to_device(bl_ctx* c, DevBuf& buf, const void* src, size_t bytes, const void** dev) {
   if (is_device_ptr(src)) {
@@ -958,6 +973,16 @@ int bl_ctx_create(int device, bl_ctx** out) {
     uy[d] = std::sin(a);
   }
   set_direction_table(ux, uy);
+  {  // shared-memory opt-in is a per-device function attribute: set it for this device
+    const int optin = (int)prop.sharedMemPerBlockOptin;
+    configure_screen_tc_kernels(optin);
+    configure_exact_kernels(optin);
+    configure_hog_kernels(optin);
+    configure_classify_kernels(optin);
+    configure_ert_kernels(optin);
+    configure_pyramid_kernels(optin);
+    CK(cudaGetLastError());
+  }
   if (const char* e = std::getenv("BL_SCREEN")) c->screen = std::strcmp(e, "fp32") == 0 ? BL_SCREEN_FP32 : BL_SCREEN_TCGEN05;
   if (const char* e = std::getenv("BL_PYR_FUSE")) c->pyr_fuse = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT"))
@@ -1070,6 +1095,7 @@ int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, d
   if (cell_px < 1) return set_err(BL_ERR_MODEL, "cell_px must be >= 1");
   if (scale_num < 1 || scale_den < 1) return set_err(BL_ERR_MODEL, "scale factor must be positive");
   TRY(use_device(c));
+  TRY(quiesce_for_upload(c));
   DetectorState& D = c->det;
   D.ready = false;
   D.thr = threshold;
@@ -1165,6 +1191,7 @@ int bl_ert_upload(bl_ctx* c, int L, int T, int K, int F, double shrinkage, const
   if (!mean_xy || ((size_t)T * K > 0 && (!leaves || (F > 0 && (!anchors || !split_params)))))
     return set_err(BL_ERR_INVALID, "null model array");
   TRY(use_device(c));
+  TRY(quiesce_for_upload(c));
   ErtState& E = c->ert;
   E.ready = false;
   const int S = (1 << F) - 1, NL = 1 << F;
@@ -1250,6 +1277,13 @@ int bl_ctx_set_face_capacity(bl_ctx* c, int faces_per_frame) {
   if (!c || faces_per_frame < 1) return set_err(BL_ERR_INVALID, "bad face capacity");
   std::lock_guard<std::mutex> lk(c->mu);
   c->face_cap_per_frame = faces_per_frame;
+  return BL_OK;
+}
+
+int bl_ctx_get_face_capacity(bl_ctx* c, int* faces_per_frame) {
+  if (!c || !faces_per_frame) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  *faces_per_frame = c->face_cap_per_frame;
   return BL_OK;
 }
 

@@ -139,11 +139,6 @@ void launch_screen(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, cons
                    const float* w32, const float* cut, Candidate* cand, unsigned long long* n_cand,
                    long long cand_cap) {
   if (Ph.sc_total <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, kScreenSmem);
-    attr = true;
-  }
   LevelBegins B{};
   B.n = Ph.n_scored;
   for (int s = 0; s < Ph.n_scored; ++s) B.b[s] = Ph.lv[s].sc_begin;
@@ -151,6 +146,10 @@ void launch_screen(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, cons
   k_screen<<<(unsigned)div_up(Ph.sc_total, kScreenWarps), kScreenWarps * 32, kScreenSmem, L.st>>>(Pd, B, feat32, w32, cut, cand,
                                                                         n_cand, cand_cap, Ph.sc_total);
   ++*L.counter;
+}
+
+void configure_classify_kernels(int optin) {  // per device, see configure_screen_tc_kernels
+  cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
 }  // namespace blb

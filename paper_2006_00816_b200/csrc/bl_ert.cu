@@ -512,15 +512,6 @@ void launch_ert_wide(const Launch& L, const ErtDev& M, const void* frames, int u
                      long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces,
                      int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err) {
   const size_t smem = sizeof(double) * 4 * M.L + sizeof(double2) + (size_t)M.K;
-  static size_t attr_u8 = 0, attr_f64 = 0;
-  size_t& attr = u8 ? attr_u8 : attr_f64;
-  if (smem > 48 * 1024 && smem > attr) {
-    if (u8)
-      cudaFuncSetAttribute(k_ert_wide<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    else
-      cudaFuncSetAttribute(k_ert_wide<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
   const int threads = (int)std::min<long long>(kWdThreads, std::max<long long>(div_up(M.K, 32), div_up(2 * M.L, 32)) * 32);
   if (u8)
     k_ert_wide<true><<<(unsigned)cap, threads, smem, L.st>>>(M, frames, w, h, pitch, fstride, face_frame, boxes,
@@ -542,15 +533,6 @@ void launch_ert_cascade(const Launch& L, const ErtDev& M, const void* frames, in
                         const int* n_faces, int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride,
                         int* err) {
   const size_t smem = sizeof(double) * kFcFaces * 2 * M.L + sizeof(double2) * kFcFaces + (size_t)kFcFaces * M.K;
-  static size_t attr_u8 = 0, attr_f64 = 0;
-  size_t& attr = u8 ? attr_u8 : attr_f64;
-  if (smem > 48 * 1024 && smem > attr) {
-    if (u8)
-      cudaFuncSetAttribute(k_ert_cascade<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    else
-      cudaFuncSetAttribute(k_ert_cascade<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
   const unsigned grid = (unsigned)div_up(cap, kFcFaces);
   if (u8)
     k_ert_cascade<true><<<grid, kFcThreads, smem, L.st>>>(M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride,
@@ -582,6 +564,13 @@ void launch_ert_finish(const Launch& L, const ErtDev& M, const int* boxes, int b
                        const int* n_faces, int cap, const double* cur, double* out_xy) {
   k_ert_finish<<<148 * 4, 256, 0, L.st>>>(M, boxes, box_stride, n_faces, cap, cur, out_xy);
   ++*L.counter;
+}
+
+void configure_ert_kernels(int optin) {  // per device, see configure_screen_tc_kernels
+  cudaFuncSetAttribute(k_ert_wide<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  cudaFuncSetAttribute(k_ert_wide<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  cudaFuncSetAttribute(k_ert_cascade<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  cudaFuncSetAttribute(k_ert_cascade<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
 }  // namespace blb

@@ -161,11 +161,6 @@ void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, c
                     const double* bias, double thr, int cell_px, const Candidate* cand,
                     const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
                     int* det_count, long long cap_pf, int* overflow) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRsSmem);
-    attr = true;
-  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -407,11 +402,6 @@ size_t nms_key_bytes() { return sizeof(NmsKey); }
 void launch_nms(const Launch& L, const DevDet* dets, const int* det_count, long long cap_pf, int n_frames,
                 double iou_thr, DevDet* kept_out, int* kept_count, void* gkeys, long long gkeys_pf) {
   if (n_frames <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_nms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nms_smem_bytes());
-    attr = true;
-  }
   k_nms<<<n_frames, 256, nms_smem_bytes(), L.st>>>(dets, det_count, cap_pf, iou_thr, kept_out, kept_count,
                                                    (NmsKey*)gkeys, gkeys_pf);
   ++*L.counter;
@@ -474,6 +464,11 @@ void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, 
   k_flatten<<<1, 1024, 0, L.st>>>(kept, kept_count, cap_pf, n_frames, offsets, flat, face_frame, meta,
                                   flat_cap, raw_overflow);
   ++*L.counter;
+}
+
+void configure_exact_kernels(int optin) {  // per device, see configure_screen_tc_kernels
+  cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  cudaFuncSetAttribute(k_nms, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
 }  // namespace blb

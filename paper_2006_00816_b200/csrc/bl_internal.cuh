@@ -189,6 +189,14 @@ void launch_resample_pair(const Launch& L, const void* src, int src_u8, int sw, 
                           long long d_fstride, int n);
 // bl_hog.cu
 void set_direction_table(const double* ux, const double* uy);
+// Per-device kernel configuration (dynamic shared-memory opt-in up to `optin` bytes), called by
+// bl_ctx_create for the context's device.
+void configure_screen_tc_kernels(int optin);
+void configure_exact_kernels(int optin);
+void configure_hog_kernels(int optin);
+void configure_classify_kernels(int optin);
+void configure_ert_kernels(int optin);
+void configure_pyramid_kernels(int optin);
 void launch_grad(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, int s_lo, int s_hi, const void* base,
                  int src_kind /*0 u8, 1 f64*/, double* fmag, uint8_t* fori);
 void launch_gradhist(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, const double* fmag,

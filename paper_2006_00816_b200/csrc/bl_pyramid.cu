@@ -228,12 +228,6 @@ void launch_resample_pair(const Launch& L, const void* src, int src_u8, int sw, 
   // region bound: floor((T - 1) * r) + 3 taps, +1 for the rounding of the computed coordinate
   const int rw = (int)((kPrTX - 1) * rx2) + 4, rh = (int)((kPrTY - 1) * ry2) + 4;
   const size_t smem = sizeof(double) * rw * rh;
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_resample_pair<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_resample_pair<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
   if (src_u8)
     k_resample_pair<uint8_t><<<grid, 256, smem, L.st>>>((const uint8_t*)src, sw, sh, s_pitch, s_fstride, mw, mh, rx1,
                                                         ry1, dst, dw, dh, d_pitch, d_fstride, rx2, ry2);
@@ -268,6 +262,11 @@ void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int s
     k_resample<double><<<grid, block, 0, L.st>>>((const double*)src, sw, sh, s_pitch, s_fstride, dst, dw, dh,
                                                   d_pitch, d_fstride, rx, ry);
   ++*L.counter;
+}
+
+void configure_pyramid_kernels(int optin) {  // per device, see configure_screen_tc_kernels
+  cudaFuncSetAttribute(k_resample_pair<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  cudaFuncSetAttribute(k_resample_pair<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
 }  // namespace blb

@@ -393,17 +393,18 @@ void launch_screen_tc(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, c
   }
   U.b[U.n] = units;
   if (units <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-    attr = true;
-  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)(units < sms ? units : sms);
   k_screen_tc<<<grid, kTcThreads, kTcSmem, L.st>>>(Pd, U, feat_tc, w_tc, cut, cand, n_cand, cand_cap, dbg_scores);
   ++*L.counter;
+}
+
+// Dynamic shared-memory opt-in of this file's kernels, for the CURRENT device (the attribute is
+// per device: bl_ctx_create calls this after cudaSetDevice, so contexts on several GPUs work).
+void configure_screen_tc_kernels(int optin) {
+  cudaFuncSetAttribute(k_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
 }  // namespace blb

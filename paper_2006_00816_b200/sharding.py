@@ -46,3 +46,15 @@ def max_over_ranks(x: float, device=None, group=None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def run_sharded(n_total: int, rank: int, world: int, make_frames, process, group=None):
+    """shard -> run -> gather: this rank builds frames [begin, end) of the global batch with
+    ``make_frames(begin, end)``, runs ``process(frames)`` (a list with one result per frame) and
+    the per-frame results are gathered onto rank 0 in global frame order.  Returns
+    (begin, end, local results, gathered list on rank 0 / None elsewhere)."""
+    begin, end = shard_range(n_total, rank, world)
+    local = list(process(make_frames(begin, end)))
+    if len(local) != end - begin:
+        raise ValueError("process() must return one result per frame")
+    return begin, end, local, gather_in_frame_order(local, rank, world, n_total, group)

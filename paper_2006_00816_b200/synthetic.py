@@ -75,3 +75,18 @@ def ring_frames_np(n, w, h, seed=0, size_frac=0.5, jitter=0.1):
         img = np.where(r <= 0.18 * size, 30.0, img)
         out[i] = np.floor(np.clip(img, 0, 255) + 0.5).astype(np.uint8)
     return out
+
+
+def ring_frame_global(i, w, h, seed=1000, size_frac=0.5, jitter=0.1):
+    """Frame `i` of a global synthetic sequence (the ring frames of ring_frames_np), generated
+    from (seed, i) alone, so any shard [begin, end) of a global batch can be built by the
+    rank that owns it and the shards concatenate to the same sequence for any world size."""
+    return ring_frames_np(1, w, h, seed=(seed, i), size_frac=size_frac, jitter=jitter)[0]
+
+
+def ring_frames_range(begin, end, w, h, seed=1000):
+    """Frames [begin, end) of the global sequence of ring_frame_global, (end-begin, h, w) u8."""
+    out = np.empty((max(0, end - begin), h, w), np.uint8)
+    for j, i in enumerate(range(begin, end)):
+        out[j] = ring_frame_global(i, w, h, seed)
+    return out
