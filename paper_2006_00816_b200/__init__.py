@@ -393,12 +393,18 @@ class Context:
     def landmarks(self, frames, frame_of_box, boxes, want_leaves=False):
         """predict_landmarks for (frame, box) pairs -> (n_boxes, L, 2) [, leaf idx (n_boxes, T*K)]."""
         a, pix, n, h, w = _frames(frames)
-        fob = _np(frame_of_box, np.int32)
-        bx = _np(boxes, np.int32).reshape(-1, 4)
-        nb = len(bx)
+        if hasattr(boxes, "data_ptr"):  # torch tensors (e.g. boxes already on the device)
+            import torch
+            fob = frame_of_box.to(torch.int32).contiguous()
+            bx = boxes.to(torch.int32).contiguous().reshape(-1, 4)
+            nb = int(bx.shape[0])
+        else:
+            fob = _np(frame_of_box, np.int32)
+            bx = _np(boxes, np.int32).reshape(-1, 4)
+            nb = len(bx)
         xy = np.zeros((nb, self.ert_L, 2))
         leaves = np.zeros((nb, self.ert_TK), np.uint8) if want_leaves else None
-        _err(lib.bl_landmarks(self._h, _addr(a), pix, n, w, h, w, w * h, fob.ctypes.data, bx.ctypes.data, nb,
+        _err(lib.bl_landmarks(self._h, _addr(a), pix, n, w, h, w, w * h, _addr(fob), _addr(bx), nb,
                               xy.ctypes.data, leaves.ctypes.data if want_leaves else None))
         return (xy, leaves) if want_leaves else xy
 

@@ -149,7 +149,7 @@ void launch_screen(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, cons
 }
 
 void configure_classify_kernels(int optin) {  // per device, see configure_screen_tc_kernels
-  cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  smem_optin(k_screen, optin);
 }
 
 }  // namespace blb

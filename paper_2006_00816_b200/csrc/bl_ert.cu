@@ -567,10 +567,10 @@ void launch_ert_finish(const Launch& L, const ErtDev& M, const int* boxes, int b
 }
 
 void configure_ert_kernels(int optin) {  // per device, see configure_screen_tc_kernels
-  cudaFuncSetAttribute(k_ert_wide<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-  cudaFuncSetAttribute(k_ert_wide<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-  cudaFuncSetAttribute(k_ert_cascade<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-  cudaFuncSetAttribute(k_ert_cascade<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  smem_optin(k_ert_wide<true>, optin);
+  smem_optin(k_ert_wide<false>, optin);
+  smem_optin(k_ert_cascade<true>, optin);
+  smem_optin(k_ert_cascade<false>, optin);
 }
 
 }  // namespace blb

@@ -467,8 +467,8 @@ void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, 
 }
 
 void configure_exact_kernels(int optin) {  // per device, see configure_screen_tc_kernels
-  cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-  cudaFuncSetAttribute(k_nms, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  smem_optin(k_rescore, optin);
+  smem_optin(k_nms, optin);
 }
 
 }  // namespace blb

@@ -189,6 +189,15 @@ void launch_resample_pair(const Launch& L, const void* src, int src_u8, int sw, 
                           long long d_fstride, int n);
 // bl_hog.cu
 void set_direction_table(const double* ux, const double* uy);
+// Dynamic shared-memory opt-in of one kernel on the current device: the largest dynamic
+// allocation the device allows next to the kernel's static shared memory.
+template <class Kernel>
+inline void smem_optin(Kernel* k, int optin) {
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, (const void*)k) != cudaSuccess) return;
+  cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes);
+}
+
 // Per-device kernel configuration (dynamic shared-memory opt-in up to `optin` bytes), called by
 // bl_ctx_create for the context's device.
 void configure_screen_tc_kernels(int optin);

@@ -265,8 +265,8 @@ void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int s
 }
 
 void configure_pyramid_kernels(int optin) {  // per device, see configure_screen_tc_kernels
-  cudaFuncSetAttribute(k_resample_pair<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-  cudaFuncSetAttribute(k_resample_pair<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  smem_optin(k_resample_pair<uint8_t>, optin);
+  smem_optin(k_resample_pair<double>, optin);
 }
 
 }  // namespace blb

@@ -404,7 +404,7 @@ void launch_screen_tc(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, c
 // Dynamic shared-memory opt-in of this file's kernels, for the CURRENT device (the attribute is
 // per device: bl_ctx_create calls this after cudaSetDevice, so contexts on several GPUs work).
 void configure_screen_tc_kernels(int optin) {
-  cudaFuncSetAttribute(k_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  smem_optin(k_screen_tc, optin);
 }
 
 }  // namespace blb
