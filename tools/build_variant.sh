@@ -14,6 +14,7 @@ for f in bl_classify bl_screen_tc bl_capi; do nvcc $FL -c $C/$f.cu -o $OUT/$f.o 
 wait
 g++ -std=c++17 -O2 -fPIC -I/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann -c $C/bl_io.cpp -o $OUT/bl_io.o
 g++ -std=c++17 -O2 -fPIC -c $C/bl_run.cpp -o $OUT/bl_run.o
+g++ -std=c++17 -O2 -fPIC -c $C/bl_multi.cpp -o $OUT/bl_multi.o
 nvcc $ARCH -shared -o $OUT/libblinkline_b200.so $OUT/*.o -Xcompiler -fPIC -lcudart_static -lrt -lpthread -ldl
 rm -f $OUT/*.o
 echo "built $OUT/libblinkline_b200.so"
