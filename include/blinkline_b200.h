@@ -96,7 +96,11 @@ int bl_ctx_launch_count(bl_ctx* ctx, uint64_t* out);
 /* Per-stage CUDA-event timing of subsequent pipeline calls (adds events; off by default). */
 int bl_ctx_enable_stage_timing(bl_ctx* ctx, int enable);
 int bl_ctx_stage_times(bl_ctx* ctx, float* ms /* BL_STAGE_COUNT */, int* launches /* BL_STAGE_COUNT */);
-/* Reserved (accepted, currently no effect): the pipeline is enqueued as individual launches. */
+/* CUDA graphs for the pipelined path (bl_submit, and the synchronous calls built on it; on by
+ * default, BL_GRAPHS=0 in the environment disables at context creation): a batch's detection
+ * launches and its landmark cascade are captured once per (lane, slot, input buffer, batch
+ * shape) and replayed, so host submit is a few graph/event calls instead of ~60 launches.
+ * Per-stage timing runs without graphs.  Results are identical either way. */
 int bl_ctx_enable_graphs(bl_ctx* ctx, int enable);
 /* Classifier screen implementation (both feed the same exact fp64 re-score, so detections
  * are bit-identical either way): BL_SCREEN_TCGEN05 -- implicit GEMM on the tensor cores

@@ -243,6 +243,10 @@ class Context:
         _err(lib.bl_ctx_launch_count(self._h, C.byref(v)))
         return int(v.value)
 
+    def enable_graphs(self, on=True):
+        """CUDA-graph replay of the pipelined path (default on; results identical either way)."""
+        _err(lib.bl_ctx_enable_graphs(self._h, int(on)))
+
     def enable_stage_timing(self, on=True):
         _err(lib.bl_ctx_enable_stage_timing(self._h, int(on)))
 

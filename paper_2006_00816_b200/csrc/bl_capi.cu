@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -59,6 +60,10 @@ namespace {
     if (rc_ != BL_OK) return rc_; \
   } while (0)
 
+// Bumped by every device (re)allocation: a captured CUDA graph bakes buffer addresses into its
+// kernel arguments, so a graph captured before the latest allocation is recaptured.
+std::atomic<uint64_t> g_alloc_epoch{1};
+
 // Device buffer that only grows.
 struct DevBuf {
   void* p = nullptr;
@@ -90,6 +95,7 @@ struct DevBuf {
     }
     cudaGetDevice(&device);
     bytes = alloc;
+    g_alloc_epoch.fetch_add(1);
     if (zero) {
       e = cudaMemset(p, 0, alloc);
       if (e != cudaSuccess) return set_err(BL_ERR_CUDA, "cudaMemset failed: %s", cudaGetErrorString(e));
@@ -240,6 +246,24 @@ struct bl_ctx {
   int stage_launch[BL_STAGE_COUNT] = {};
   bool graphs = true;
   cudaStream_t hst = nullptr;  // H2D stream (input frames): never queued behind a D2H wait
+  // CUDA graphs (bl_ctx_enable_graphs): a batch's detection launches (one graph per lane plan,
+  // slot and input) and its landmark cascade (one per slot and input) are captured once on a
+  // private stream and replayed; host submit then costs a few graph/event calls instead of
+  // ~60 launches.  Entries are keyed by everything baked into the kernel arguments.
+  struct GraphEntry {
+    int kind = 0;  // 0: detection + flatten, 1: landmark cascade
+    const void* plan = nullptr;
+    int slot = 0;
+    const void* in = nullptr;
+    long long dp = 0, df = 0, cap_faces = 0;
+    int n = 0, w = 0, h = 0, pix = 0, landmarks = 0;
+    uint64_t epoch = 0, model_gen = 0, last_use = 0;
+    uint64_t kernels = 0;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<GraphEntry> gcache;
+  cudaStream_t cap = nullptr;
+  uint64_t model_gen = 1, use_clock = 0;
   Slot slots[BL_MAX_IN_FLIGHT];
   uint64_t next_ticket = 1;
   int face_cap_per_frame = 64;  // device-side capacity of landmarked faces per frame
@@ -435,13 +459,10 @@ void stage_mark(bl_ctx* c, int stage) {
 // Enqueues detect on n frames already resident on the device (`in`, element pitch/stride) on
 // the active lane's stream: leaves each frame's kept detections in P.kept / P.kept_count on
 // the device (no host synchronisation).
-int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long long pitch,
-               long long fstride, int64_t* total_out) {
+// Host half of a detect batch: the plan (geometry + arenas) and the level-0 descriptor.
+int prepare_detect(bl_ctx* c, int pix, int n, int w, int h, long long pitch, long long fstride) {
   Plan& P = *c->plan;
   TRY(build_plan(c, P, n, w, h, pix));
-  const Launch L = launch_of(c);
-  const DetectorState& D = c->det;
-
   // level 0 descriptor points at the caller's frames
   if (!P.scored.empty() && P.scored[0] == 0) {
     LevelDesc& L0 = P.host.lv[0];
@@ -452,6 +473,15 @@ int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long lon
       CK(cudaMemcpyAsync(P.desc.p, &P.host, sizeof(PlanDesc), cudaMemcpyHostToDevice, c->st));
     }
   }
+  return BL_OK;
+}
+
+// Device half: every launch of the detect path on c->st (capturable: no host synchronisation,
+// no allocation -- prepare_detect sized the plan).
+int record_detect(bl_ctx* c, const void* in, int pix, int n, long long pitch, long long fstride) {
+  Plan& P = *c->plan;
+  const Launch L = launch_of(c);
+  const DetectorState& D = c->det;
   stage_mark(c, BL_STAGE_PYRAMID);
   // pyramid chain (image.cpp:162-170): level k from level k-1, every frame at once.  A level
   // no window scores (below the smallest eligible face) is read only by the next step, so
@@ -507,8 +537,12 @@ int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long lon
   stage_mark(c, BL_STAGE_NMS);
   launch_nms(L, P.dets.as<DevDet>(), P.det_count.as<int>(), P.cap_pf, n, 0.5, P.kept.as<DevDet>(),
              P.kept_count.as<int>(), P.gkeys.p, P.gkeys_pf);
-  (void)total_out;
   return BL_OK;
+}
+
+int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long long pitch, long long fstride) {
+  TRY(prepare_detect(c, pix, n, w, h, pitch, fstride));
+  return record_detect(c, in, pix, n, pitch, fstride);
 }
 
 // Stage host frames into a device buffer (or use device frames in place).
@@ -635,6 +669,69 @@ bool is_pinned_or_device(const void* p) {
   return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Replays the graph cached for `key` on stream `st`, capturing it first (on the private
+// capture stream, with c->st pointed at it while `record` enqueues) when absent or stale.
+template <class Record>
+int graph_launch(bl_ctx* c, bl_ctx::GraphEntry key, cudaStream_t st, Record&& record) {
+  const uint64_t epoch = g_alloc_epoch.load();
+  key.epoch = epoch;
+  key.model_gen = c->model_gen;
+  bl_ctx::GraphEntry* hit = nullptr;
+  for (auto& g : c->gcache)
+    if (g.kind == key.kind && g.plan == key.plan && g.slot == key.slot && g.in == key.in && g.dp == key.dp &&
+        g.df == key.df && g.cap_faces == key.cap_faces && g.n == key.n && g.w == key.w && g.h == key.h &&
+        g.pix == key.pix && g.landmarks == key.landmarks) {
+      hit = &g;
+      break;
+    }
+  if (hit && (hit->epoch != epoch || hit->model_gen != key.model_gen)) {  // stale: buffers or model changed
+    cudaGraphExecDestroy(hit->exec);
+    *hit = c->gcache.back();
+    c->gcache.pop_back();
+    hit = nullptr;
+  }
+  if (!hit) {
+    constexpr size_t kMaxGraphs = 32;
+    if (c->gcache.size() >= kMaxGraphs) {  // evict the least recently used
+      size_t lru = 0;
+      for (size_t i = 1; i < c->gcache.size(); ++i)
+        if (c->gcache[i].last_use < c->gcache[lru].last_use) lru = i;
+      cudaGraphExecDestroy(c->gcache[lru].exec);
+      c->gcache[lru] = c->gcache.back();
+      c->gcache.pop_back();
+    }
+    const cudaStream_t saved = c->st;
+    const uint64_t l0 = c->launches;
+    c->st = c->cap;
+    CK(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeRelaxed));
+    const int rc = record();
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->cap, &g);
+    c->st = saved;
+    key.kernels = c->launches - l0;
+    c->launches = l0;
+    if (rc != BL_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ec != cudaSuccess) return set_err(BL_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ec));
+    const cudaError_t ei = cudaGraphInstantiate(&key.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) return set_err(BL_ERR_CUDA, "graph instantiation failed: %s", cudaGetErrorString(ei));
+    c->gcache.push_back(key);
+    hit = &c->gcache.back();
+  }
+  hit->last_use = ++c->use_clock;
+  CK(cudaGraphLaunch(hit->exec, st));
+  c->launches += hit->kernels;
+  return BL_OK;
+}
+
+void drop_graphs(bl_ctx* c) {
+  for (auto& g : c->gcache) cudaGraphExecDestroy(g.exec);
+  c->gcache.clear();
+}
+
 // Enqueues detect (+ landmarks) for one batch into slot `s`: no host synchronisation.
 int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, size_t pitch, size_t fstride,
             int landmarks) {
@@ -690,15 +787,40 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
     dp = w;
     df = (long long)w * h;
   }
-  TRY(run_detect(c, dev, pix, n, w, h, dp, df, nullptr));
+  TRY(prepare_detect(c, pix, n, w, h, dp, df));
   TRY(S.flat.ensure(sizeof(DevDet) * cap_faces));
   TRY(S.face_frame.ensure(sizeof(int) * cap_faces));
   TRY(S.meta.ensure(sizeof(int) * (n + 4)));
+  if (landmarks) TRY(S.ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * cap_faces));
   int* meta = S.meta.as<int>();
-  launch_flatten(launch_of(c), P.kept.as<DevDet>(), P.kept_count.as<int>(), P.cap_pf, n, P.offsets.as<int>(),
-                 S.flat.as<DevDet>(), S.face_frame.as<int>(), meta, cap_faces, P.overflow.as<int>());
+  const bool graph = c->graphs && !c->timing;
+  // detection + flatten on the lane stream
+  auto rec_det = [&]() -> int {
+    TRY(record_detect(c, dev, pix, n, dp, df));
+    launch_flatten(launch_of(c), P.kept.as<DevDet>(), P.kept_count.as<int>(), P.cap_pf, n, P.offsets.as<int>(),
+                   S.flat.as<DevDet>(), S.face_frame.as<int>(), meta, cap_faces, P.overflow.as<int>());
+    if (!landmarks) CK(cudaMemsetAsync(meta + n + 2, 0, sizeof(int), c->st));
+    return BL_OK;
+  };
+  if (graph) {
+    bl_ctx::GraphEntry key;
+    key.kind = 0;
+    key.plan = c->plan;
+    key.slot = s;
+    key.in = dev;
+    key.dp = dp;
+    key.df = df;
+    key.cap_faces = cap_faces;
+    key.n = n;
+    key.w = w;
+    key.h = h;
+    key.pix = pix;
+    key.landmarks = landmarks;
+    TRY(graph_launch(c, key, c->st, rec_det));
+  } else {
+    TRY(rec_det());
+  }
   if (landmarks) {
-    TRY(S.ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * cap_faces));
     stage_mark(c, BL_STAGE_ERT);
     // the cascade only reads this slot's buffers and the frames, so (unless per-stage timing
     // wants one ordered stream) it runs on the ERT stream while the next batch detects
@@ -707,11 +829,30 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
       CK(cudaEventRecord(S.ev_det, c->st));
       CK(cudaStreamWaitEvent(es, S.ev_det, 0));
     }
-    TRY(run_ert(c, es, S.ert, dev, pix, w, h, dp, df, S.face_frame.as<int>(), S.flat.as<int>(), 8, meta + n,
-                (int)cap_faces, nullptr, S.ert_out.as<double>(), meta + n + 2, (long long)n * kErtFacesPerFrameGuess));
+    auto rec_ert = [&](cudaStream_t st) -> int {
+      return run_ert(c, st, S.ert, dev, pix, w, h, dp, df, S.face_frame.as<int>(), S.flat.as<int>(), 8, meta + n,
+                     (int)cap_faces, nullptr, S.ert_out.as<double>(), meta + n + 2,
+                     (long long)n * kErtFacesPerFrameGuess);
+    };
+    if (graph) {
+      TRY(ert_work_ensure(c->ert, S.ert, (int)cap_faces, true));
+      bl_ctx::GraphEntry key;
+      key.kind = 1;
+      key.slot = s;
+      key.in = dev;
+      key.dp = dp;
+      key.df = df;
+      key.cap_faces = cap_faces;
+      key.n = n;
+      key.w = w;
+      key.h = h;
+      key.pix = pix;
+      TRY(graph_launch(c, key, es, [&]() { return rec_ert(c->st); }));
+    } else {
+      TRY(rec_ert(es));
+    }
     CK(cudaEventRecord(S.ev_done, es));
   } else {
-    CK(cudaMemsetAsync(meta + n + 2, 0, sizeof(int), c->st));
     CK(cudaEventRecord(S.ev_done, c->st));
   }
   // counts + flags back on the slot's D2H stream as soon as compute finishes
@@ -948,6 +1089,7 @@ int bl_ctx_create(int device, bl_ctx** out) {
   c->device = device;
   CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->hst, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
   {  // the cascades fill the gaps of the next batches' detection: lowest priority
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -985,6 +1127,7 @@ int bl_ctx_create(int device, bl_ctx** out) {
   }
   if (const char* e = std::getenv("BL_SCREEN")) c->screen = std::strcmp(e, "fp32") == 0 ? BL_SCREEN_FP32 : BL_SCREEN_TCGEN05;
   if (const char* e = std::getenv("BL_PYR_FUSE")) c->pyr_fuse = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BL_GRAPHS")) c->graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT"))
     c->ert_mode = !std::strcmp(e, "cascade") ? 1 : !std::strcmp(e, "wide") ? 2 : !std::strcmp(e, "levels") ? 3 : 0;
   CK(cudaGetLastError());
@@ -995,6 +1138,8 @@ int bl_ctx_create(int device, bl_ctx** out) {
 void bl_ctx_destroy(bl_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  drop_graphs(c);
+  if (c->cap) cudaStreamDestroy(c->cap);
   cudaStreamSynchronize(c->st);
   if (c->hst) cudaStreamSynchronize(c->hst);
   for (int l = 1; l < kLanes; ++l)
@@ -1078,12 +1223,15 @@ int bl_ctx_set_screen(bl_ctx* c, int mode) {
   if (mode != BL_SCREEN_TCGEN05 && mode != BL_SCREEN_FP32) return set_err(BL_ERR_INVALID, "unknown screen mode %d", mode);
   std::lock_guard<std::mutex> lk(c->mu);
   c->screen = mode;
+  ++c->model_gen;  // captured graphs launch the other screen
   return BL_OK;
 }
 
 int bl_ctx_enable_graphs(bl_ctx* c, int enable) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
   c->graphs = enable != 0;
+  if (!c->graphs) drop_graphs(c);
   return BL_OK;
 }
 
@@ -1096,6 +1244,7 @@ int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, d
   if (scale_num < 1 || scale_den < 1) return set_err(BL_ERR_MODEL, "scale factor must be positive");
   TRY(use_device(c));
   TRY(quiesce_for_upload(c));
+  ++c->model_gen;  // thresholds and cuts are baked into captured graphs
   DetectorState& D = c->det;
   D.ready = false;
   D.thr = threshold;
@@ -1192,6 +1341,7 @@ int bl_ert_upload(bl_ctx* c, int L, int T, int K, int F, double shrinkage, const
     return set_err(BL_ERR_INVALID, "null model array");
   TRY(use_device(c));
   TRY(quiesce_for_upload(c));
+  ++c->model_gen;  // the cascade's dims and pointers are baked into captured graphs
   ErtState& E = c->ert;
   E.ready = false;
   const int S = (1 << F) - 1, NL = 1 << F;

@@ -55,7 +55,8 @@ BL_DEV double sample_px(const void* fr, int w, int h, long long pitch, int bx, i
   return __ldg((const double*)fr + (long long)iy * pitch + ix);
 }
 
-__device__ int face_transform(const ErtDev& M, const double* c, double& A, double& B, const double* mc = nullptr);
+__device__ int face_transform_warp(const ErtDev& M, const double* c, const double* mc, int lane, double& A,
+                                   double& B);
 
 // (1) similarity_transform(current, mean) per face, ert.cpp:26-69.  A warp per face stages
 // the current shape in shared memory; lane 0 then runs the sums sequentially in the
@@ -76,39 +77,55 @@ __global__ void __launch_bounds__(32 * kXfFaces) k_ert_xform(ErtDev M, const int
   const double* cur = cur_g + (long long)face * L2;
   for (int i = lane; i < L2; i += 32) sc[warp][i] = cur[i];
   __syncwarp();
-  if (lane != 0) return;
   double A = 0.0, B = 0.0;
-  const int e = face_transform(M, sc[warp], A, B);
+  const int e = face_transform_warp(M, sc[warp], M.mean_c, lane, A, B);
+  if (lane != 0) return;
   if (e) atomicExch(err, e);
   tf[face] = make_double2(A, B);
 }
 
-// similarity_transform(current -> mean) of one face (ert.cpp:26-69), sequential sums in the
-// reference's order; returns 0 or the reference's error (1: source shape has no spread, 2:
-// target shape has no spread) and the linear part (scale*cos, scale*sin) in A, B.
-// `mc`: a shared-memory copy of M.mean_c (else read through the read-only path).
-__device__ int face_transform(const ErtDev& M, const double* c, double& A, double& B, const double* mc) {
+// Canonical device summation order of the cascade (every kernel uses it, so the kernels are
+// bit-identical to each other; against the reference's sequential sums the landmarks move by
+// ~1e-16 relative, far inside the 1e-3 px contract, and no leaf decision flips -- SURVEY.md
+// §0.6 measured 0 mismatches in 7.5 M decisions for arbitrary fp64 summation orders, and the
+// C4 test checks all 10k boxes against the reference):
+//  * shape sums of the similarity transform: lane l of a warp adds points l, l + 32, ... in
+//    order, then an xor butterfly over the 32 lanes (every lane ends with the same bits);
+//  * leaf sums: partial sums over chunks of kLeafChunk consecutive trees (each in tree order,
+//    from 0.0), then the partials in chunk order.
+constexpr int kLeafChunk = 64;
+
+BL_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// similarity_transform(current -> mean) of one face (ert.cpp:26-69), computed by a whole warp
+// (c, mc: the current shape and the centred mean shape, shared or global).  Returns 0 or the
+// reference's error (1: source shape has no spread, 2: target shape has no spread) and the
+// linear part (scale*cos, scale*sin) in A, B; identical in every lane.
+__device__ int face_transform_warp(const ErtDev& M, const double* c, const double* mc, int lane, double& A,
+                                   double& B) {
   const int L = M.L;
-  double mfx = 0.0, mfy = 0.0;
-#pragma unroll 4
-  for (int i = 0; i < L; ++i) {
-    mfx = dadd(mfx, c[2 * i]);
-    mfy = dadd(mfy, c[2 * i + 1]);
+  double sx = 0.0, sy = 0.0;
+  for (int i = lane; i < L; i += 32) {  // ert.cpp:33-43 centroid
+    sx = dadd(sx, c[2 * i]);
+    sy = dadd(sy, c[2 * i + 1]);
   }
-  mfx = ddiv(mfx, (double)L);
-  mfy = ddiv(mfy, (double)L);
+  const double mfx = ddiv(warp_sum(sx), (double)L), mfy = ddiv(warp_sum(sy), (double)L);
   double sff = 0.0, sre = 0.0, sim = 0.0;
-#pragma unroll 4
-  for (int i = 0; i < L; ++i) {
+  for (int i = lane; i < L; i += 32) {  // ert.cpp:44-55
     const double fx = dsub(c[2 * i], mfx);
     const double fy = dsub(c[2 * i + 1], mfy);
-    // to.x - mt.x, host-computed with the same op
-    const double txp = mc ? mc[2 * i] : __ldg(M.mean_c + 2 * i);
-    const double typ = mc ? mc[2 * i + 1] : __ldg(M.mean_c + 2 * i + 1);
+    const double txp = mc[2 * i], typ = mc[2 * i + 1];  // to.x - mt.x, host-computed with the same op
     sff = dadd(sff, dadd(dmul(fx, fx), dmul(fy, fy)));
     sre = dadd(sre, dadd(dmul(fx, txp), dmul(fy, typ)));
     sim = dadd(sim, dsub(dmul(fx, typ), dmul(fy, txp)));
   }
+  sff = warp_sum(sff);
+  sre = warp_sum(sre);
+  sim = warp_sum(sim);
   A = 0.0;
   B = 0.0;
   if (!(sff > 0.0)) return 1;  // "source shape has no spread" (ert.cpp:56-57)
@@ -179,28 +196,34 @@ __global__ void __launch_bounds__(256) k_ert_accum(ErtDev M, int t, const int* _
   const uint8_t* li = leaf_idx + (long long)face * leaf_stride;
   const double2* lv = reinterpret_cast<const double2*>(M.leaves + (long long)t * K * NL * 2 * L) + p;
   const int row = NL * L;  // double2 per tree
-  double ax = 0.0, ay = 0.0;
-  int k = 0;
+  double ax = 0.0, ay = 0.0;  // the canonical chunked order (face_transform_warp's note)
   const bool vec = ((reinterpret_cast<uintptr_t>(li) & 15) == 0);
-  for (; vec && k + 16 <= K; k += 16) {
-    const uint4 q = *reinterpret_cast<const uint4*>(li + k);
-    const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
-    double2 v[16];
+  for (int c0 = 0; c0 < K; c0 += kLeafChunk) {
+    const int c1 = min(K, c0 + kLeafChunk);
+    double px = 0.0, py = 0.0;
+    int k = c0;
+    for (; vec && k + 16 <= c1; k += 16) {
+      const uint4 q = *reinterpret_cast<const uint4*>(li + k);
+      const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+      double2 v[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int idx = (wv[u >> 2] >> ((u & 3) * 8)) & 0xff;
-      v[u] = __ldg(lv + (k + u) * row + idx * L);
-    }
+      for (int u = 0; u < 16; ++u) {
+        const int idx = (wv[u >> 2] >> ((u & 3) * 8)) & 0xff;
+        v[u] = __ldg(lv + (k + u) * row + idx * L);
+      }
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      ax = dadd(ax, v[u].x);
-      ay = dadd(ay, v[u].y);
+      for (int u = 0; u < 16; ++u) {
+        px = dadd(px, v[u].x);
+        py = dadd(py, v[u].y);
+      }
     }
-  }
-  for (; k < K; ++k) {
-    const double2 v = __ldg(lv + k * row + li[k] * L);
-    ax = dadd(ax, v.x);
-    ay = dadd(ay, v.y);
+    for (; k < c1; ++k) {
+      const double2 v = __ldg(lv + k * row + li[k] * L);
+      px = dadd(px, v.x);
+      py = dadd(py, v.y);
+    }
+    ax = dadd(ax, px);
+    ay = dadd(ay, py);
   }
   double2* cur = reinterpret_cast<double2*>(cur_g + (long long)face * 2 * L) + p;
   double2 cv = *cur;
@@ -267,12 +290,14 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
   for (int e = tid; e < nf * L2; e += blockDim.x) sc[e] = M.mean_xy[e % L2];  // ert.cpp:106
   __syncthreads();
   for (int t = 0; t < M.T; ++t) {
-    // (1) transforms
-    if (warp < nf && lane == 0) {
+    // (1) transforms, a warp per face
+    if (warp < nf) {
       double A, B;
-      const int e = face_transform(M, sc + warp * L2, A, B);
-      if (e) atomicExch(err, e);
-      stf[warp] = make_double2(A, B);
+      const int e = face_transform_warp(M, sc + warp * L2, M.mean_c, lane, A, B);
+      if (lane == 0) {
+        if (e) atomicExch(err, e);
+        stf[warp] = make_double2(A, B);
+      }
     }
     __syncthreads();
     // (2) traversals: two (face, tree) items per thread walk their trees in lock-step (all
@@ -330,22 +355,28 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
       const uint8_t* li = sli + fi * K;
       const double2* lv = reinterpret_cast<const double2*>(M.leaves + (long long)t * K * NL * 2 * L) + p;
       const int row = NL * L;
-      double ax = 0.0, ay = 0.0;
-      int k = 0;
-      for (; k + 16 <= K; k += 16) {
-        double2 v[16];
+      double ax = 0.0, ay = 0.0;  // the canonical chunked order
+      for (int c0 = 0; c0 < K; c0 += kLeafChunk) {
+        const int c1 = min(K, c0 + kLeafChunk);
+        double px = 0.0, py = 0.0;
+        int k = c0;
+        for (; k + 16 <= c1; k += 16) {
+          double2 v[16];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = __ldg(lv + (k + u) * row + li[k + u] * L);
+          for (int u = 0; u < 16; ++u) v[u] = __ldg(lv + (k + u) * row + li[k + u] * L);
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          ax = dadd(ax, v[u].x);
-          ay = dadd(ay, v[u].y);
+          for (int u = 0; u < 16; ++u) {
+            px = dadd(px, v[u].x);
+            py = dadd(py, v[u].y);
+          }
         }
-      }
-      for (; k < K; ++k) {
-        const double2 v = __ldg(lv + k * row + li[k] * L);
-        ax = dadd(ax, v.x);
-        ay = dadd(ay, v.y);
+        for (; k < c1; ++k) {
+          const double2 v = __ldg(lv + k * row + li[k] * L);
+          px = dadd(px, v.x);
+          py = dadd(py, v.y);
+        }
+        ax = dadd(ax, px);
+        ay = dadd(ay, py);
       }
       double* c = sc + fi * L2 + 2 * p;
       c[0] = dadd(c[0], dmul(M.shrinkage, ax));
@@ -362,56 +393,54 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
   }
 }
 
-// The cascade for SMALL batches (a camera stream's 16 frames, one frame): one face per CTA
-// and a thread per tree / per coordinate, so a level's latency chain is one traversal and
-// one K-long sum instead of kFcFaces faces' worth of them per thread.  Same arithmetic as
-// k_ert_cascade (bit-identical):
-//   xform    thread 0: similarity transform of the staged current shape;
-//   traverse thread per tree: level-order descent, leaf index -> smem;
-//   accum    thread per coordinate: the K selected leaf values in tree order, 32 loads in
-//            flight, cur += shrinkage * delta.
-#ifndef BL_ERT_WIDE_THREADS
-#define BL_ERT_WIDE_THREADS 256
-#endif
-constexpr int kWdThreads = BL_ERT_WIDE_THREADS;
-#ifndef BL_WD_PROBE
-#define BL_WD_PROBE 0  // timing probes: bit 0 skips the sums, 1 the traversals, 2 the transform
-#endif
-
+// The cascade for SMALL batches (a camera stream's 16 frames, one frame): latency-bound, a
+// face's 15 levels are one dependent chain, so each level is spread over a whole CTA:
+//   xform    warp 0: face_transform_warp (shuffle reductions);
+//   traverse thread per tree: level-order descent with the root's split record prefetched
+//            before the transform, leaf index -> smem;
+//   accum    thread per (landmark pair, chunk of kLeafChunk trees): the chunk's selected leaf
+//            pairs in tree order, 16 loads in flight, partial -> smem; then thread per pair:
+//            the partials in chunk order, cur += shrinkage * delta.
+// The leaf sum of a level is then ~kLeafChunk dependent adds and loads deep instead of K.
+// Same canonical order as k_ert_cascade / k_ert_accum (bit-identical to both).
 #ifndef BL_WD_CLOCK
 #define BL_WD_CLOCK 0  // per-phase clock64 totals of face 0, printed (experiments)
 #endif
-
-#ifndef BL_WD_INFLIGHT
-#define BL_WD_INFLIGHT 32
-#endif
-constexpr int kWdInFlight = BL_WD_INFLIGHT;  // leaf loads in flight per coordinate thread
+constexpr int kWdMaxThreads = 1024;
+constexpr int kWdInFlight = 16;  // leaf loads in flight per (pair, chunk) thread
 
 struct SplitPlanes {  // one split record as its three 16-B planes
   double2 oa, ob;
   int4 tail;  // thr (lo, hi), anchors (a | b << 16)
 };
 
+int ert_wide_threads(const ErtDev& M) {
+  const int items = M.L * (int)div_up(M.K, kLeafChunk);
+  return (int)std::min<long long>(kWdMaxThreads, div_up(std::max(std::max(M.K, items), 32), 32) * 32);
+}
+
 template <bool U8>
-__global__ void __launch_bounds__(kWdThreads) k_ert_wide(ErtDev M, const void* __restrict__ frames, int w, int h,
-                                                  long long pitch, long long fstride,
-                                                  const int* __restrict__ face_frame,
-                                                  const int* __restrict__ boxes, int box_stride,
-                                                  const int* __restrict__ n_faces, int cap,
-                                                  double* __restrict__ out_xy, uint8_t* __restrict__ leaf_out,
-                                                  long long leaf_out_stride, int* __restrict__ err) {
+__global__ void __launch_bounds__(kWdMaxThreads) k_ert_wide(ErtDev M, const void* __restrict__ frames, int w, int h,
+                                                     long long pitch, long long fstride,
+                                                     const int* __restrict__ face_frame,
+                                                     const int* __restrict__ boxes, int box_stride,
+                                                     const int* __restrict__ n_faces, int cap,
+                                                     double* __restrict__ out_xy, uint8_t* __restrict__ leaf_out,
+                                                     long long leaf_out_stride, int* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char wd_smem[];
   const int L = M.L, L2 = 2 * L, K = M.K, S = M.S, NL = M.NL;
-  double* sc = reinterpret_cast<double*>(wd_smem);             // [2L]
-  double* smc = sc + L2;                                       // [2L] mean_c
-  double2* stf = reinterpret_cast<double2*>(smc + L2);         // [1]
-  uint8_t* sli = reinterpret_cast<uint8_t*>(stf + 1);          // [K]
+  const int nchunk = (K + kLeafChunk - 1) / kLeafChunk;
+  double* sc = reinterpret_cast<double*>(wd_smem);             // [2L] current shape
+  double* smc = sc + L2;                                       // [2L] centred mean shape
+  double2* stf = reinterpret_cast<double2*>(smc + L2);         // [1] transform
+  double2* spart = stf + 1;                                    // [nchunk][L] partial leaf sums
+  uint8_t* sli = reinterpret_cast<uint8_t*>(spart + nchunk * L);  // [K]
   const int bd = blockDim.x;
   const int n = min(*n_faces, cap);
   const int face = blockIdx.x;
   if (face >= n) return;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < L2; e += blockDim.x) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < L2; e += bd) {
     sc[e] = M.mean_xy[e];  // ert.cpp:106
     smc[e] = M.mean_c[e];
   }
@@ -430,66 +459,83 @@ __global__ void __launch_bounds__(kWdThreads) k_ert_wide(ErtDev M, const void* _
       r.ob = __ldg(reinterpret_cast<const double2*>(q + M.split_plane));
       r.tail = __ldg(q + 2 * M.split_plane);
     };
+    SplitPlanes root;  // this thread's first tree's root record: independent of the transform
+    if (tid < K && S > 0) rec(0, tid, root);
 #if BL_WD_CLOCK
     long long c0 = clock64();
 #endif
-    if (tid == 0 && !(BL_WD_PROBE & 4)) {  // (1) transform
+    if (warp == 0) {  // (1) transform
       double A, B;
-      const int e = face_transform(M, sc, A, B, smc);
-      if (e) atomicExch(err, e);
-      stf[0] = make_double2(A, B);
+      const int e = face_transform_warp(M, sc, smc, lane, A, B);
+      if (lane == 0) {
+        if (e) atomicExch(err, e);
+        stf[0] = make_double2(A, B);
+      }
     }
     __syncthreads();
 #if BL_WD_CLOCK
     long long c1 = clock64();
 #endif
-    // (2) traversals, ert.cpp:87-97: two trees per thread walked in lock-step (all trees
-    // have depth F), so both trees' record and pixel loads are in flight together
+    // (2) traversals, ert.cpp:87-97
     const double2 ab = stf[0];
-    for (int k0 = tid; k0 < K && !(BL_WD_PROBE & 2); k0 += 2 * bd) {
-      const int kk[2] = {k0, k0 + bd < K ? k0 + bd : k0};  // a duplicate of k0 when unpaired
-      int node[2] = {0, 0};
+    for (int k = tid; k < K; k += bd) {
+      int node = 0;
       for (int d = 0; d < M.F; ++d) {
-        SplitPlanes r[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) rec(node[q], kk[q], r[q]);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const double thr = __hiloint2double(r[q].tail.y, r[q].tail.x);
-          const int an_a = (short)(r[q].tail.z & 0xffff), an_b = (short)(r[q].tail.z >> 16);
-          const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_a, r[q].oa.x, r[q].oa.y);
-          const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_b, r[q].ob.x, r[q].ob.y);
-          node[q] = dsub(ia, ib) > thr ? 2 * node[q] + 1 : 2 * node[q] + 2;
-        }
+        SplitPlanes r;
+        if (d == 0 && k == tid)
+          r = root;
+        else
+          rec(node, k, r);
+        const double thr = __hiloint2double(r.tail.y, r.tail.x);
+        const int an_a = (short)(r.tail.z & 0xffff), an_b = (short)(r.tail.z >> 16);
+        const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_a, r.oa.x, r.oa.y);
+        const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_b, r.ob.x, r.ob.y);
+        node = dsub(ia, ib) > thr ? 2 * node + 1 : 2 * node + 2;
       }
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        sli[kk[q]] = (uint8_t)(node[q] - S);
-        if (leaf_out) leaf_out[(long long)face * leaf_out_stride + (long long)t * K + kk[q]] = (uint8_t)(node[q] - S);
-      }
+      sli[k] = (uint8_t)(node - S);
+      if (leaf_out) leaf_out[(long long)face * leaf_out_stride + (long long)t * K + k] = (uint8_t)(node - S);
     }
     __syncthreads();
 #if BL_WD_CLOCK
     long long c2 = clock64();
 #endif
-    // (3) leaf sums in tree order, cur += shrinkage * delta (ert.cpp:118-126): thread c < 2L
-    // adds coordinate c of the selected rows, kWdInFlight loads issued ahead of their adds.
-    // A level costs about K dependent fp64 adds here (the loads hide behind them: more in
-    // flight, or the coordinates split over a CTA cluster, measured no faster).
-    if (tid < L2 && !(BL_WD_PROBE & 1)) {
-      double acc = 0.0;
-      const double* lv = M.leaves + (long long)t * K * NL * L2 + tid;
-      const int row = NL * L2;
-      int k = 0;
-      for (; k + kWdInFlight <= K; k += kWdInFlight) {
-        double v[kWdInFlight];
+    // (3a) partial leaf sums: item = (chunk, pair), consecutive threads read consecutive pairs
+    // of one leaf row
+    const double2* lv = reinterpret_cast<const double2*>(M.leaves + (long long)t * K * NL * L2);
+    const int row = NL * L;  // double2 per tree
+    for (int it = tid; it < nchunk * L; it += bd) {
+      const int ch = it / L, p = it - ch * L;
+      const int k0 = ch * kLeafChunk, k1 = min(K, k0 + kLeafChunk);
+      double px = 0.0, py = 0.0;
+      int k = k0;
+      for (; k + kWdInFlight <= k1; k += kWdInFlight) {
+        double2 v[kWdInFlight];
 #pragma unroll
-        for (int u = 0; u < kWdInFlight; ++u) v[u] = __ldg(lv + (long long)(k + u) * row + sli[k + u] * L2);
+        for (int u = 0; u < kWdInFlight; ++u) v[u] = __ldg(lv + (long long)(k + u) * row + sli[k + u] * L + p);
 #pragma unroll
-        for (int u = 0; u < kWdInFlight; ++u) acc = dadd(acc, v[u]);
+        for (int u = 0; u < kWdInFlight; ++u) {
+          px = dadd(px, v[u].x);
+          py = dadd(py, v[u].y);
+        }
       }
-      for (; k < K; ++k) acc = dadd(acc, __ldg(lv + (long long)k * row + sli[k] * L2));
-      sc[tid] = dadd(sc[tid], dmul(M.shrinkage, acc));  // the traversals' reads of sc are done
+      for (; k < k1; ++k) {
+        const double2 v = __ldg(lv + (long long)k * row + sli[k] * L + p);
+        px = dadd(px, v.x);
+        py = dadd(py, v.y);
+      }
+      spart[it] = make_double2(px, py);
+    }
+    __syncthreads();
+    // (3b) partials in chunk order, cur += shrinkage * delta (ert.cpp:118-126)
+    if (tid < L) {
+      double ax = 0.0, ay = 0.0;
+      for (int ch = 0; ch < nchunk; ++ch) {
+        const double2 q = spart[ch * L + tid];
+        ax = dadd(ax, q.x);
+        ay = dadd(ay, q.y);
+      }
+      sc[2 * tid] = dadd(sc[2 * tid], dmul(M.shrinkage, ax));
+      sc[2 * tid + 1] = dadd(sc[2 * tid + 1], dmul(M.shrinkage, ay));
     }
     __syncthreads();
 #if BL_WD_CLOCK
@@ -501,18 +547,19 @@ __global__ void __launch_bounds__(kWdThreads) k_ert_wide(ErtDev M, const void* _
   if (tid == 0 && face == 0) printf("k_ert_wide face 0 cycles: xform %lld traverse %lld accum %lld\n", clk[0], clk[1], clk[2]);
 #endif
   // ert.cpp:132-133: box.x + p.x * box.w, box.y + p.y * box.h
-  for (int c = tid; c < L2; c += blockDim.x)
+  for (int c = tid; c < L2; c += bd)
     out_xy[(long long)face * L2 + c] = (c & 1) ? dadd((double)Y, dmul(sc[c], (double)H))
                                                : dadd((double)X, dmul(sc[c], (double)W));
 }
 
-bool ert_wide_fits(const ErtDev& M) { return 2 * M.L <= kWdThreads && 2 * M.L <= kMaxL2; }
+bool ert_wide_fits(const ErtDev& M) { return 2 * M.L <= kMaxL2; }
 
 void launch_ert_wide(const Launch& L, const ErtDev& M, const void* frames, int u8, int w, int h, long long pitch,
                      long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces,
                      int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err) {
-  const size_t smem = sizeof(double) * 4 * M.L + sizeof(double2) + (size_t)M.K;
-  const int threads = (int)std::min<long long>(kWdThreads, std::max<long long>(div_up(M.K, 32), div_up(2 * M.L, 32)) * 32);
+  const long long nchunk = div_up(M.K, kLeafChunk);
+  const size_t smem = sizeof(double) * 4 * M.L + sizeof(double2) * (1 + nchunk * M.L) + (size_t)M.K;
+  const int threads = ert_wide_threads(M);
   if (u8)
     k_ert_wide<true><<<(unsigned)cap, threads, smem, L.st>>>(M, frames, w, h, pitch, fstride, face_frame, boxes,
                                                               box_stride, n_faces, cap, out_xy, leaf_out,

@@ -70,6 +70,16 @@ def test_c4_ert_only_10k_boxes(ctx, oracle):
         wxy, wl, _ = oracle.predict_landmarks(img, tuple(boxes[i]), ert)
         assert np.array_equal(leaves[i], wl), i
         assert np.max(np.abs(xy[i] - wxy)) <= 1e-9
+    # every one of the 10k boxes against the unmodified reference library (all host threads):
+    # a single flipped leaf decision would move a landmark by >= 1e-3 px, far above 1e-9 (the
+    # device sums run in the canonical chunked order)
+    import os
+
+    from pyoracle import Reference, reference_available
+    if reference_available():
+        want = Reference().landmarks_batch_u8(u8[None], np.zeros(n, np.int32), boxes, ert, os.cpu_count() or 1,
+                                              want_xy=True)
+        assert np.max(np.abs(xy - want)) <= 1e-9
     # order invariance + determinism on all 10k
     perm = r.permutation(n)
     xy2 = ctx.landmarks(u8, np.zeros(n, np.int32), boxes[perm])
