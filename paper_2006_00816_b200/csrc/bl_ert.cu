@@ -130,11 +130,20 @@ __device__ int face_transform_warp(const ErtDev& M, const double* c, const doubl
   B = 0.0;
   if (!(sff > 0.0)) return 1;  // "source shape has no spread" (ert.cpp:56-57)
   const double a = ddiv(sre, sff), b = ddiv(sim, sff);
-  const double scale = hypot(a, b);
+  // ert.cpp:60-67, the three libm chains on different lanes (same functions, same results):
+  // lane 2 scale = hypot(a, b); lanes 0 / 1 rot = atan2(b, a) then cos / sin
+  double v;
+  if (lane == 2) {
+    v = hypot(a, b);
+  } else {
+    const double rot = atan2(b, a);
+    v = lane == 1 ? sin(rot) : cos(rot);
+  }
+  const double scale = __shfl_sync(0xffffffffu, v, 2);
+  const double cr = __shfl_sync(0xffffffffu, v, 0), sr = __shfl_sync(0xffffffffu, v, 1);
   if (!(scale > 0.0)) return 2;  // "target shape has no spread" (ert.cpp:62-63)
-  const double rot = atan2(b, a);
-  A = dmul(scale, cos(rot));
-  B = dmul(scale, sin(rot));
+  A = dmul(scale, cr);
+  B = dmul(scale, sr);
   return 0;
 }
 
@@ -406,7 +415,7 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
 #ifndef BL_WD_CLOCK
 #define BL_WD_CLOCK 0  // per-phase clock64 totals of face 0, printed (experiments)
 #endif
-constexpr int kWdMaxThreads = 1024;
+constexpr int kWdMaxThreads = 640;  // 96 registers per thread
 constexpr int kWdInFlight = 16;  // leaf loads in flight per (pair, chunk) thread
 
 struct SplitPlanes {  // one split record as its three 16-B planes
@@ -479,18 +488,28 @@ __global__ void __launch_bounds__(kWdMaxThreads) k_ert_wide(ErtDev M, const void
     // (2) traversals, ert.cpp:87-97
     const double2 ab = stf[0];
     for (int k = tid; k < K; k += bd) {
+      // both children's records are loaded while a node's pixels are sampled, so a descent
+      // step waits on its pixel loads only
       int node = 0;
+      SplitPlanes r;
+      if (k == tid)
+        r = root;
+      else
+        rec(0, k, r);
       for (int d = 0; d < M.F; ++d) {
-        SplitPlanes r;
-        if (d == 0 && k == tid)
-          r = root;
-        else
-          rec(node, k, r);
+        SplitPlanes c1, c2;
+        const bool more = d + 1 < M.F;
+        if (more) {
+          rec(2 * node + 1, k, c1);
+          rec(2 * node + 2, k, c2);
+        }
         const double thr = __hiloint2double(r.tail.y, r.tail.x);
         const int an_a = (short)(r.tail.z & 0xffff), an_b = (short)(r.tail.z >> 16);
         const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_a, r.oa.x, r.oa.y);
         const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_b, r.ob.x, r.ob.y);
-        node = dsub(ia, ib) > thr ? 2 * node + 1 : 2 * node + 2;
+        const bool right = dsub(ia, ib) > thr;
+        node = right ? 2 * node + 1 : 2 * node + 2;
+        if (more) r = right ? c1 : c2;
       }
       sli[k] = (uint8_t)(node - S);
       if (leaf_out) leaf_out[(long long)face * leaf_out_stride + (long long)t * K + k] = (uint8_t)(node - S);

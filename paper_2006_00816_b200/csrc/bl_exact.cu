@@ -256,6 +256,7 @@ BL_DEV unsigned long long pack2(int hi, int lo) {
 
 constexpr int kNmsSmemKeys = 512;    // keys sorted in shared memory up to this count
 constexpr int kNmsSmemKept = 256;    // kept boxes cached in shared memory
+constexpr int kNmsSmallFrames = 32;  // batches up to this many frames use k_nms_small
 
 // One CTA per frame: bitonic sort of the frame's detections, then the greedy scan by
 // warp 0 (kept boxes checked 32 at a time with __any_sync).
@@ -263,10 +264,11 @@ __global__ void __launch_bounds__(256) k_nms(const DevDet* __restrict__ dets,
                                              const int* __restrict__ det_count, long long cap_pf,
                                              double iou_thr, DevDet* __restrict__ kept_out,
                                              int* __restrict__ kept_count, NmsKey* __restrict__ gkeys,
-                                             long long gkeys_pf) {
+                                             long long gkeys_pf, int only_above) {
   extern __shared__ unsigned char nms_smem[];
   const int f = blockIdx.x;
   const int n = (int)min((long long)det_count[f], cap_pf);
+  if (n <= only_above) return;  // k_nms_small's frame
   const DevDet* D = dets + (long long)f * cap_pf;
   if (n == 0) {
     if (threadIdx.x == 0) kept_count[f] = 0;
@@ -389,6 +391,157 @@ __global__ void __launch_bounds__(256) k_nms(const DevDet* __restrict__ dets,
   if (lane == 0) kept_count[f] = kept;
 }
 
+// NMS for SMALL batches (one frame, a 16-frame camera stream): one 1024-thread CTA per frame
+// with up to kNmsSmallMax detections sorted in shared memory, and the greedy scan
+// (detector.cpp:130-140) in rounds over the whole CTA: the next <= 32 boxes of the order that
+// no kept box suppresses so far are resolved among themselves in order (a 32 x 32 overlap
+// matrix, one IoU per thread, then a 32-step bit scan), and every later box is tested against
+// the round's newly kept boxes in parallel.  Rounds ~ kept / batch, not n, so a frame with
+// a thousand raw detections and a handful of faces takes a few microseconds.
+constexpr int kNmsSmallMax = 2048;
+constexpr int kNmsSmallThreads = 1024;
+
+size_t nms_small_smem_bytes() {
+  return sizeof(NmsKey) * kNmsSmallMax + sizeof(uint32_t) * (kNmsSmallMax / 32 + 32 + 32 + 8);
+}
+
+__global__ void __launch_bounds__(kNmsSmallThreads) k_nms_small(const DevDet* __restrict__ dets,
+                                                                const int* __restrict__ det_count, long long cap_pf,
+                                                                double iou_thr, DevDet* __restrict__ kept_out,
+                                                                int* __restrict__ kept_count) {
+  extern __shared__ __align__(16) unsigned char nsm[];
+  NmsKey* keys = reinterpret_cast<NmsKey*>(nsm);
+  DevDet* sorted = reinterpret_cast<DevDet*>(nsm);  // gathered in place of the keys
+  uint32_t* supp = reinterpret_cast<uint32_t*>(nsm + sizeof(NmsKey) * kNmsSmallMax);  // processed / suppressed
+  int* cand = reinterpret_cast<int*>(supp + kNmsSmallMax / 32);                         // [32]
+  uint32_t* ovl = reinterpret_cast<uint32_t*>(cand + 32);                               // [32]
+  int* ctl = reinterpret_cast<int*>(ovl + 32);  // [0] candidates, [1] kept so far, [2] keep mask, [3] next p
+  const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = (int)min((long long)det_count[f], cap_pf);
+  if (n > kNmsSmallMax) return;  // k_nms's frame
+  if (n == 0) {
+    if (tid == 0) kept_count[f] = 0;
+    return;
+  }
+  const DevDet* D = dets + (long long)f * cap_pf;
+  int Pn = 1;
+  while (Pn < n) Pn <<= 1;
+  for (int i = tid; i < Pn; i += blockDim.x) {
+    NmsKey k;
+    if (i < n) {
+      const DevDet d = D[i];
+      k.score = d.score;
+      k.t1 = pack2(d.y, d.x);
+      k.t2 = pack2(d.scale_index, d.rotation_index);
+      k.idx = i;
+    } else {
+      k.score = -DBL_MAX;
+      k.t1 = k.t2 = ~0ull;
+      k.idx = 0x7fffffff;
+    }
+    k.pad = 0;
+    keys[i] = k;
+  }
+  for (int i = tid; i < kNmsSmallMax / 32; i += blockDim.x) supp[i] = 0u;
+  __syncthreads();
+  for (int k = 2; k <= Pn; k <<= 1) {  // bitonic sort, detector.cpp:125-129 order
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < Pn; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const NmsKey a = keys[i], b = keys[ixj];
+          const bool up = (i & k) == 0;
+          if (up ? before(b, a) : before(a, b)) {
+            keys[i] = b;
+            keys[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < n; i += blockDim.x) {  // each thread reads its own key before overwriting it
+    const int idx = keys[i].idx;
+    sorted[i] = D[idx];
+  }
+  if (tid == 0) {
+    ctl[1] = 0;
+    ctl[3] = 0;
+  }
+  __syncthreads();
+  DevDet* out = kept_out + (long long)f * cap_pf;
+  const int nwords = (n + 31) >> 5;
+  while (true) {
+    const int p = ctl[3];
+    if (warp == 0) {  // the next <= 32 unprocessed boxes at or after p, in order
+      const int w = (p >> 5) + lane;
+      uint32_t free_bits = 0;
+      if (w < nwords) {
+        free_bits = ~supp[w];
+        if (w == (p >> 5)) free_bits &= ~0u << (p & 31);
+        if (w == nwords - 1 && (n & 31)) free_bits &= (1u << (n & 31)) - 1u;
+      }
+      const int cnt = __popc(free_bits);
+      int pre = cnt;  // inclusive prefix over lanes
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += v;
+      }
+      int pos = pre - cnt;
+      while (free_bits && pos < 32) {
+        cand[pos++] = (w << 5) + __ffs(free_bits) - 1;
+        free_bits &= free_bits - 1;
+      }
+      const int tot = __shfl_sync(0xffffffffu, pre, 31);
+      if (lane == 0) ctl[0] = min(tot, 32);
+    }
+    __syncthreads();
+    const int nc = ctl[0];
+    if (nc == 0) break;
+    {  // overlap matrix of the candidates: warp a, lane b < a
+      const int a = warp, b = lane;
+      bool o = false;
+      if (a < nc && b < a) o = iou_exceeds(sorted[cand[b]], sorted[cand[a]], iou_thr);
+      const uint32_t m = __ballot_sync(0xffffffffu, o);
+      if (lane == 0 && a < 32) ovl[a] = m;
+    }
+    __syncthreads();
+    if (tid == 0) {  // resolve the batch in order; candidates become processed
+      uint32_t keep = 0;
+      int kept = ctl[1];
+      for (int a = 0; a < nc; ++a) {
+        if (!(ovl[a] & keep)) {
+          keep |= 1u << a;
+          out[kept++] = sorted[cand[a]];
+        }
+        atomicOr(&supp[cand[a] >> 5], 1u << (cand[a] & 31));
+      }
+      ctl[1] = kept;
+      ctl[2] = (int)keep;
+      ctl[3] = cand[nc - 1] + 1;
+    }
+    __syncthreads();
+    const uint32_t keep = (uint32_t)ctl[2];
+    const int np = ctl[3];
+    for (int j = np + tid; j < n; j += blockDim.x) {  // later boxes against the round's kept boxes
+      if ((supp[j >> 5] >> (j & 31)) & 1u) continue;
+      const DevDet dj = sorted[j];
+      uint32_t kk = keep;
+      while (kk) {
+        const int a = __ffs(kk) - 1;
+        kk &= kk - 1;
+        if (iou_exceeds(sorted[cand[a]], dj, iou_thr)) {
+          atomicOr(&supp[j >> 5], 1u << (j & 31));
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) kept_count[f] = ctl[1];
+}
+
 size_t nms_smem_bytes() { return sizeof(NmsKey) * kNmsSmemKeys + sizeof(DevDet) * kNmsSmemKept; }
 
 long long nms_gkeys_per_frame(long long cap_pf) {
@@ -402,8 +555,19 @@ size_t nms_key_bytes() { return sizeof(NmsKey); }
 void launch_nms(const Launch& L, const DevDet* dets, const int* det_count, long long cap_pf, int n_frames,
                 double iou_thr, DevDet* kept_out, int* kept_count, void* gkeys, long long gkeys_pf) {
   if (n_frames <= 0) return;
+  if (n_frames <= kNmsSmallFrames) {  // latency path; k_nms takes only frames above its limit
+    k_nms_small<<<n_frames, kNmsSmallThreads, nms_small_smem_bytes(), L.st>>>(dets, det_count, cap_pf, iou_thr,
+                                                                               kept_out, kept_count);
+    ++*L.counter;
+    if (cap_pf > kNmsSmallMax) {
+      k_nms<<<n_frames, 256, nms_smem_bytes(), L.st>>>(dets, det_count, cap_pf, iou_thr, kept_out, kept_count,
+                                                       (NmsKey*)gkeys, gkeys_pf, kNmsSmallMax);
+      ++*L.counter;
+    }
+    return;
+  }
   k_nms<<<n_frames, 256, nms_smem_bytes(), L.st>>>(dets, det_count, cap_pf, iou_thr, kept_out, kept_count,
-                                                   (NmsKey*)gkeys, gkeys_pf);
+                                                   (NmsKey*)gkeys, gkeys_pf, -1);
   ++*L.counter;
 }
 
@@ -469,6 +633,7 @@ void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, 
 void configure_exact_kernels(int optin) {  // per device, see configure_screen_tc_kernels
   smem_optin(k_rescore, optin);
   smem_optin(k_nms, optin);
+  smem_optin(k_nms_small, optin);
 }
 
 }  // namespace blb
