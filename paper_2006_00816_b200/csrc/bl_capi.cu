@@ -218,6 +218,7 @@ struct Slot {
 constexpr int kLanes = 4;
 constexpr int kLanesLarge = 2;
 constexpr long long kSmallBatchPx = 16LL << 20;
+constexpr long long kChainMaxPx = 1LL << 19;  // batches up to this many pixels: k_pyramid_chain (C1 yes, C2 no: measured)
 
 struct bl_ctx {
   int device = 0;
@@ -272,6 +273,7 @@ struct bl_ctx {
   // by BL_ERT=wide|cascade|levels (experiments)
   int ert_mode = 0;
   bool pyr_fuse = true;  // fused resample pairs over unscored levels (BL_PYR_FUSE=0 disables)
+  bool pyr_chain = true;  // one cooperative launch for a small batch's chain (BL_PYR_CHAIN=0 disables)
 };
 
 namespace {
@@ -488,7 +490,31 @@ int record_detect(bl_ctx* c, const void* in, int pix, int n, long long pitch, lo
   // the two steps run fused (k_resample_pair) and that level never reaches HBM.
   std::vector<char> is_scored(P.n_levels + 1, 0);
   for (int k : P.scored) is_scored[k] = 1;
-  for (int k = 1; k < P.n_levels; ++k) {
+  // small batches: the whole chain in one cooperative launch (launch latency, not bandwidth,
+  // bounds a one-frame pyramid)
+  const bool chain = c->pyr_chain && (long long)n * P.w * P.h <= kChainMaxPx && P.n_levels > 2;
+  if (chain) {
+    PyrChain C{};
+    C.n_levels = P.n_levels;
+    C.n_frames = n;
+    C.src0 = in;
+    C.s0_pitch = pitch;
+    C.s0_fstride = fstride;
+    for (int k = 0; k < P.n_levels; ++k) {
+      C.lw[k] = P.lw[k];
+      C.lh[k] = P.lh[k];
+      if (k >= 1) {
+        C.lv[k] = P.arena.as<double>() + P.arena_off[k];
+        C.lpitch[k] = P.lpitch[k];
+        C.lfstride[k] = (long long)P.lpitch[k] * P.lh[k];
+        C.rx[k] = double(P.lw[k - 1]) / P.lw[k];  // image.cpp:136-137
+        C.ry[k] = double(P.lh[k - 1]) / P.lh[k];
+      }
+    }
+    if (const int e = launch_pyramid_chain(L, C, pix == BL_PIX_U8))
+      return set_err(BL_ERR_CUDA, "pyramid chain launch failed: %s", cudaGetErrorString((cudaError_t)e));
+  }
+  for (int k = 1; k < P.n_levels && !chain; ++k) {
     const void* src = k == 1 ? in : (const void*)(P.arena.as<double>() + P.arena_off[k - 1]);
     const int src_u8 = (k == 1 && pix == BL_PIX_U8);
     const long long sp = k == 1 ? pitch : P.lpitch[k - 1];
@@ -1128,6 +1154,7 @@ int bl_ctx_create(int device, bl_ctx** out) {
   if (const char* e = std::getenv("BL_SCREEN")) c->screen = std::strcmp(e, "fp32") == 0 ? BL_SCREEN_FP32 : BL_SCREEN_TCGEN05;
   if (const char* e = std::getenv("BL_PYR_FUSE")) c->pyr_fuse = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_GRAPHS")) c->graphs = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BL_PYR_CHAIN")) c->pyr_chain = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT"))
     c->ert_mode = !std::strcmp(e, "cascade") ? 1 : !std::strcmp(e, "wide") ? 2 : !std::strcmp(e, "levels") ? 3 : 0;
   CK(cudaGetLastError());

@@ -184,6 +184,17 @@ struct Launch {
 void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
                      long long s_fstride, double* dst, int dw, int dh, long long d_pitch, long long d_fstride, int n);
 bool resample_pair_fits(int sw, int sh, int mw, int mh, int dw, int dh);
+// The whole pyramid chain (levels 1 .. n_levels-1) in one cooperative launch (small batches).
+struct PyrChain {
+  int n_levels, n_frames;
+  const void* src0;
+  long long s0_pitch, s0_fstride;
+  int lw[kMaxLevels], lh[kMaxLevels];
+  double* lv[kMaxLevels];  // level k >= 1: frame 0, pixel (0, 0)
+  long long lpitch[kMaxLevels], lfstride[kMaxLevels];
+  double rx[kMaxLevels], ry[kMaxLevels];  // step k: double(w_{k-1}) / w_k (image.cpp:136-137)
+};
+int launch_pyramid_chain(const Launch& L, const PyrChain& C, int src_u8);
 void launch_resample_pair(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,
                           long long s_fstride, int mw, int mh, double* dst, int dw, int dh, long long d_pitch,
                           long long d_fstride, int n);

@@ -8,7 +8,10 @@
 //
 // Roofline: HBM-bound.  Algorithmic bytes per output pixel: 8 B written + the source
 // level read once (1 B/px for u8 level 0, 8 B/px otherwise, 1.44 source px per output px).
+#include <cooperative_groups.h>
 #include <stdint.h>
+
+#include <algorithm>
 
 #include "bl_internal.cuh"
 
@@ -262,6 +265,82 @@ void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int s
     k_resample<double><<<grid, block, 0, L.st>>>((const double*)src, sw, sh, s_pitch, s_fstride, dst, dw, dh,
                                                   d_pitch, d_fstride, rx, ry);
   ++*L.counter;
+}
+
+// The whole chain for SMALL batches (one frame, a 16-frame camera stream): each step is too
+// small to fill the GPU and its cost is launch + drain latency, so every level is produced
+// by ONE cooperative launch, a grid-stride pass per level with a grid barrier between levels
+// (level k reads level k-1).  Per pixel the same arithmetic as k_resample (bit-identical).
+namespace cg = cooperative_groups;
+
+template <typename T0>
+__global__ void __launch_bounds__(256) k_pyramid_chain(const PyrChain C) {
+  cg::grid_group grid = cg::this_grid();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int k = 1; k < C.n_levels; ++k) {
+    const int sw = C.lw[k - 1], sh = C.lh[k - 1], dw = C.lw[k], dh = C.lh[k];
+    const double rx = C.rx[k], ry = C.ry[k];
+    const double xmax = (double)(sw - 1), ymax = (double)(sh - 1);
+    const long long total = (long long)C.n_frames * dh * dw;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int f = (int)(i / ((long long)dh * dw));
+      const int rem = (int)(i - (long long)f * dh * dw);
+      const int y = rem / dw, x = rem - (rem / dw) * dw;
+      double sx = dsub(dmul(dadd((double)x, 0.5), rx), 0.5);  // image.cpp:139-149
+      sx = sx < 0.0 ? 0.0 : (xmax < sx ? xmax : sx);
+      const int x0 = (int)sx, x1 = min(x0 + 1, sw - 1);
+      const double fx = dsub(sx, (double)x0), gx = dsub(1.0, fx);
+      double sy = dsub(dmul(dadd((double)y, 0.5), ry), 0.5);
+      sy = sy < 0.0 ? 0.0 : (ymax < sy ? ymax : sy);
+      const int y0 = (int)sy, y1 = min(y0 + 1, sh - 1);
+      const double fy = dsub(sy, (double)y0), gy = dsub(1.0, fy);
+      double a, b, c, e;
+      if (k == 1) {
+        const T0* s = reinterpret_cast<const T0*>(C.src0) + (long long)f * C.s0_fstride;
+        a = (double)__ldg(s + y0 * C.s0_pitch + x0);
+        b = (double)__ldg(s + y0 * C.s0_pitch + x1);
+        c = (double)__ldg(s + y1 * C.s0_pitch + x0);
+        e = (double)__ldg(s + y1 * C.s0_pitch + x1);
+      } else {  // written by this launch: plain loads (not the read-only path)
+        const double* s = C.lv[k - 1] + (long long)f * C.lfstride[k - 1];
+        const long long p = C.lpitch[k - 1];
+        a = s[y0 * p + x0];
+        b = s[y0 * p + x1];
+        c = s[y1 * p + x0];
+        e = s[y1 * p + x1];
+      }
+      const double top = dadd(dmul(a, gx), dmul(b, fx));  // image.cpp:150-152
+      const double bot = dadd(dmul(c, gx), dmul(e, fx));
+      C.lv[k][(long long)f * C.lfstride[k] + (long long)y * C.lpitch[k] + x] = dadd(dmul(top, gy), dmul(bot, fy));
+    }
+    if (k + 1 < C.n_levels) grid.sync();
+  }
+}
+
+int launch_pyramid_chain(const Launch& L, const PyrChain& C, int src_u8) {
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* fn = src_u8 ? (const void*)k_pyramid_chain<uint8_t> : (const void*)k_pyramid_chain<double>;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+  long long most = 0;  // the largest level's pixels: no more CTAs than it needs
+  for (int k = 1; k < C.n_levels; ++k) most = std::max(most, (long long)C.n_frames * C.lw[k] * C.lh[k]);
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((long long)sms * std::min(per_sm, 1),
+                                                                               div_up(most, 256)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = L.st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = src_u8 ? cudaLaunchKernelEx(&cfg, k_pyramid_chain<uint8_t>, C)
+                               : cudaLaunchKernelEx(&cfg, k_pyramid_chain<double>, C);
+  ++*L.counter;
+  return e == cudaSuccess ? 0 : (int)e;
 }
 
 void configure_pyramid_kernels(int optin) {  // per device, see configure_screen_tc_kernels

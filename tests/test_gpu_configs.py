@@ -132,3 +132,28 @@ def test_fused_unscored_levels_bit_identical(monkeypatch, pattern_model):
     assert sum(len(d) for d in out["1"][0]) > 0
     for k in range(len(frames)):
         assert np.array_equal(out["1"][0][k], out["0"][0][k]) and np.array_equal(out["1"][1][k], out["0"][1][k])
+
+
+@pytest.mark.parametrize("w,h,n,f64", [(640, 480, 1, False), (320, 240, 16, False), (333, 250, 3, True),
+                                       (161, 97, 2, False)])
+def test_pyramid_chain_bit_identical(monkeypatch, oracle, pattern_model, w, h, n, f64):
+    """Small batches build the pyramid in one cooperative launch (k_pyramid_chain, grid barrier
+    between levels); detections and landmarks equal the per-level chain's (BL_PYR_CHAIN=0) bit
+    for bit, and the oracle's."""
+    import paper_2006_00816_b200 as bl
+    frames = ring_frames_np(n, w, h, seed=w + n)
+    if f64:
+        frames = frames.astype(np.float64) + 0.25
+    ert = random_ert(T=2, K=40, F=4, seed=72)
+    out = {}
+    for chain in ("1", "0"):
+        monkeypatch.setenv("BL_PYR_CHAIN", chain)
+        c = bl.Context(0)
+        c.upload_detector(pattern_model)
+        c.upload_ert(ert)
+        out[chain] = c.detect_landmarks(frames)
+        c.close()
+    for k in range(n):
+        assert np.array_equal(out["1"][0][k], out["0"][0][k]) and np.array_equal(out["1"][1][k], out["0"][1][k])
+    img = frames[0].astype(np.float64)
+    assert np.array_equal(out["1"][0][0], oracle.detect_faces(img, pattern_model))
