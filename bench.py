@@ -538,7 +538,38 @@ def measure_configs(args, torch, bl, ctx, stream, det, ert):
                                   "kind": "reference", "sample": single["sample"],
                                   "median_ms_per_frame": single["median_ms"]}}
     out["C4"] = measure_c4(torch, bl, ctx, stream, ert, ref, cores)
+    out["run"] = measure_run(bl, ctx, det, ert, ref, cores)
     return out
+
+
+def measure_run(bl, ctx, det, ert, ref, cores, n=256, batch=64):
+    """run() end to end (pipeline.cpp:396-404): a directory of n 640x480 PGM frames -> decode,
+    detect, the best face's 68 landmarks, EAR trace.  Ours: bl_run (persistent decoder thread
+    into pinned buffers, BL_MAX_IN_FLIGHT batches in flight); reference: its pipelined run()
+    with all usable host threads as workers.  Wall clock, PGM decode included on both sides."""
+    import shutil
+    import tempfile
+    d = tempfile.mkdtemp(prefix="bl_run_")
+    try:
+        for i, f in enumerate(tiled_frames(n, W, H, distinct=32, seed=91)):
+            bl.write_pgm(os.path.join(d, f"frame_{i:06d}.pgm"), f)
+        ctx.run(d, 30.0, batch_size=batch)  # warm-up (plans, graphs, page cache)
+        t0 = time.perf_counter()
+        ours = ctx.run(d, 30.0, batch_size=batch)
+        t_ours = time.perf_counter() - t0
+        ref.run(d, det, ert, 30.0, pipelined=cores, batch_size=16)  # warm-up
+        t0 = time.perf_counter()
+        want = ref.run(d, det, ert, 30.0, pipelined=cores, batch_size=16)
+        t_ref = time.perf_counter() - t0
+        same = bool(np.array_equal(ours["detections"], want["detections"]) and
+                    np.array_equal(ours["frames"]["face_found"], want["face_found"]))
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    return {"workload": f"run(): {n} PGM frames {W}x{H}, decode + detect + best-face landmarks + EAR trace",
+            "value": round(n / t_ours, 1), "unit": "frames/s", "batch_size": batch,
+            "reference": {"value": round(n / t_ref, 2), "unit": "frames/s", "workers": cores,
+                          "kind": "reference run(), pipelined"},
+            "detections_identical": same}
 
 
 def measure_c4(torch, bl, ctx, stream, ert, ref, cores):
@@ -679,6 +710,8 @@ def run_reference(args):
 
 
 def main():
+    import faulthandler
+    faulthandler.enable()
     a = parse()
     sys.path.insert(0, ROOT)
     if a.gpus > 1 and "WORLD_SIZE" not in os.environ and a.impl == "ours":

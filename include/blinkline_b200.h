@@ -152,6 +152,12 @@ int bl_detect_landmarks(bl_ctx* ctx, const void* frames, int pixel_type, int n, 
  * flight, so later batches' H2D, the landmark cascade of an earlier one (its own stream) and
  * result copies overlap detection.  Tickets are collected in submission order. */
 #define BL_MAX_IN_FLIGHT 4
+/* with_landmarks: 0 = detection only; BL_LANDMARKS_ALL = every kept detection (landmarks of
+ * bl_collect aligned with `out`); BL_LANDMARKS_BEST = the first (best) detection of each frame
+ * only, as the reference's run() does (pipeline.cpp:167-190): bl_collect's landmarks then hold
+ * one row per FRAME (n x L x 2), rows of frames without a detection undefined. */
+#define BL_LANDMARKS_ALL 1
+#define BL_LANDMARKS_BEST 2
 int bl_submit(bl_ctx* ctx, const void* frames, int pixel_type, int n, int w, int h, size_t pitch,
               size_t frame_stride, int with_landmarks, uint64_t* ticket);
 int bl_collect(bl_ctx* ctx, uint64_t ticket, bl_detection* out, int64_t cap, int32_t* counts,
@@ -160,6 +166,10 @@ int bl_collect(bl_ctx* ctx, uint64_t ticket, bl_detection* out, int64_t cap, int
  * synchronous calls grow it automatically, bl_collect reports BL_ERR_CAPACITY. */
 int bl_ctx_set_face_capacity(bl_ctx* ctx, int faces_per_frame);
 int bl_ctx_get_face_capacity(bl_ctx* ctx, int* faces_per_frame);
+/* Page-locked host memory (cudaMallocHost) for frames and results: H2D / D2H then run at full
+ * PCIe rate and overlap device work. */
+int bl_host_alloc(size_t bytes, void** out);
+void bl_host_free(void* p);
 
 /* ------------------------------------------------------------- multi-device ---- */
 /* Frame sharding over several GPUs in one process (replaces the reference's

@@ -309,7 +309,7 @@ class Reference(_Base):
             return {"n_detections": nd[:k], "face_found": ff[:k], "faces": faces[:k], "landmarks": lm_buf[:k],
                     "ears": ears[:k], "detections": dets[:int(tot[0])], "baselines": base}
         finally:
-            self.lib.ref_ert_destroy(h)
+            pass  # h is owned by the ert_handle cache (destroying it here left a dangling entry)
 
     prefix = "ref_"
 

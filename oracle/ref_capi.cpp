@@ -684,6 +684,10 @@ int ref_run(const char* dir, const double* weights, const double* biases, double
     cfg.batch_size = std::size_t(batch_size);
     cfg.detect_workers = pipelined ? 2 : 1;
     cfg.landmark_workers = pipelined ? 2 : 1;
+    if (pipelined >= 2) {  // `pipelined` = total worker threads (the CPU-baseline timing uses all cores)
+      cfg.detect_workers = std::max(1, (2 * pipelined) / 3);
+      cfg.landmark_workers = std::max(1, pipelined - cfg.detect_workers);
+    }
     const RunOutput out = run(dir, hog, static_cast<RefErt*>(ert)->model, fps, cfg);
     const int n = int(out.results.size());
     *n_frames = n;

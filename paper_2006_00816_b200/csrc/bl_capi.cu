@@ -191,7 +191,7 @@ struct ErtWork {
 // BL_MAX_IN_FLIGHT slots let later batches' H2D and detection overlap an earlier batch's
 // landmark cascade and result copies (bl_submit/collect).
 struct Slot {
-  DevBuf input, flat, face_frame, meta, ert_out;
+  DevBuf input, flat, face_frame, meta, ert_out, best, best_frame;
   ErtWork ert;                  // the slot's cascade runs on the ERT stream, beside the next detect
   cudaEvent_t ev_det = nullptr; // detections flattened: the ERT stream may start
   int* h_meta = nullptr;
@@ -779,6 +779,8 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
   long long dp = 0, df = 0;
   const size_t es = pix == BL_PIX_U8 ? 1 : 8;
   const long long cap_faces = std::max<long long>(1, (long long)n * c->face_cap_per_frame);
+  const bool best_only = landmarks == BL_LANDMARKS_BEST;
+  const long long lm_rows = best_only ? n : cap_faces;  // landmark rows the cascade writes
   // Every slot is sized together on first use (and on growth), so a pipeline's later slots
   // never allocate -- a synchronising cudaMalloc -- while earlier batches are in flight.
   for (Slot& o : c->slots) {
@@ -788,8 +790,12 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
     TRY(o.meta.ensure(sizeof(int) * (n + 4)));
     TRY(ensure_pinned(reinterpret_cast<void*&>(o.h_meta), o.h_meta_cap, sizeof(int) * (n + 4)));
     if (landmarks) {
-      TRY(o.ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * cap_faces));
-      TRY(ert_work_ensure(c->ert, o.ert, (int)cap_faces, true));
+      TRY(o.ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * lm_rows));
+      TRY(ert_work_ensure(c->ert, o.ert, (int)lm_rows, true));
+    }
+    if (best_only) {
+      TRY(o.best.ensure(sizeof(DevDet) * n));
+      TRY(o.best_frame.ensure(sizeof(int) * n));
     }
   }
   if (is_device_ptr(frames)) {
@@ -817,14 +823,14 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
   TRY(S.flat.ensure(sizeof(DevDet) * cap_faces));
   TRY(S.face_frame.ensure(sizeof(int) * cap_faces));
   TRY(S.meta.ensure(sizeof(int) * (n + 4)));
-  if (landmarks) TRY(S.ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * cap_faces));
   int* meta = S.meta.as<int>();
   const bool graph = c->graphs && !c->timing;
   // detection + flatten on the lane stream
   auto rec_det = [&]() -> int {
     TRY(record_detect(c, dev, pix, n, dp, df));
     launch_flatten(launch_of(c), P.kept.as<DevDet>(), P.kept_count.as<int>(), P.cap_pf, n, P.offsets.as<int>(),
-                   S.flat.as<DevDet>(), S.face_frame.as<int>(), meta, cap_faces, P.overflow.as<int>());
+                   S.flat.as<DevDet>(), S.face_frame.as<int>(), meta, cap_faces, P.overflow.as<int>(),
+                   best_only ? S.best.as<DevDet>() : nullptr, best_only ? S.best_frame.as<int>() : nullptr);
     if (!landmarks) CK(cudaMemsetAsync(meta + n + 2, 0, sizeof(int), c->st));
     return BL_OK;
   };
@@ -856,15 +862,19 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
       CK(cudaStreamWaitEvent(es, S.ev_det, 0));
     }
     auto rec_ert = [&](cudaStream_t st) -> int {
+      if (best_only)  // the face of each frame only (run(), pipeline.cpp:171-190): row f = frame f
+        return run_ert(c, st, S.ert, dev, pix, w, h, dp, df, S.best_frame.as<int>(), S.best.as<int>(), 8,
+                       meta + n + 3, n, nullptr, S.ert_out.as<double>(), meta + n + 2, n);
       return run_ert(c, st, S.ert, dev, pix, w, h, dp, df, S.face_frame.as<int>(), S.flat.as<int>(), 8, meta + n,
                      (int)cap_faces, nullptr, S.ert_out.as<double>(), meta + n + 2,
                      (long long)n * kErtFacesPerFrameGuess);
     };
     if (graph) {
-      TRY(ert_work_ensure(c->ert, S.ert, (int)cap_faces, true));
+      TRY(ert_work_ensure(c->ert, S.ert, (int)lm_rows, true));
       bl_ctx::GraphEntry key;
       key.kind = 1;
       key.slot = s;
+      key.landmarks = landmarks;
       key.in = dev;
       key.dp = dp;
       key.df = df;
@@ -929,7 +939,8 @@ int collect(bl_ctx* c, int s, bl_detection* out, int64_t cap, int32_t* counts, i
     return set_err(BL_ERR_CAPACITY, "output capacity %lld < %lld detections", (long long)cap, (long long)tot);
   stage_mark(c, BL_STAGE_D2H);
   const size_t bd = sizeof(bl_detection) * tot;
-  const size_t bl = S.landmarks && landmarks ? sizeof(double) * 2 * c->ert.dev.L * tot : 0;
+  const int64_t lm_rows = S.landmarks == BL_LANDMARKS_BEST ? S.n : tot;  // best-only: one row per frame
+  const size_t bl = S.landmarks && landmarks ? sizeof(double) * 2 * c->ert.dev.L * lm_rows : 0;
   const bool direct_d = !out || is_pinned_or_device(out);
   const bool direct_l = !bl || is_pinned_or_device(landmarks);
   const size_t need = (direct_d ? 0 : bd) + (direct_l ? 0 : bl) + 64;
@@ -1457,6 +1468,17 @@ int bl_ctx_set_face_capacity(bl_ctx* c, int faces_per_frame) {
   return BL_OK;
 }
 
+int bl_host_alloc(size_t bytes, void** out) {
+  if (!out) return set_err(BL_ERR_INVALID, "null argument");
+  *out = nullptr;
+  CK(cudaMallocHost(out, std::max<size_t>(bytes, 1)));
+  return BL_OK;
+}
+
+void bl_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int bl_ctx_get_face_capacity(bl_ctx* c, int* faces_per_frame) {
   if (!c || !faces_per_frame) return set_err(BL_ERR_INVALID, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
@@ -1470,6 +1492,8 @@ int bl_submit(bl_ctx* c, const void* frames, int pixel_type, int n, int w, int h
   std::lock_guard<std::mutex> lk(c->mu);
   if (!c->det.ready) return set_err(BL_ERR_STATE, "no detector model uploaded");
   if (with_landmarks && !c->ert.ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
+  if (with_landmarks < 0 || with_landmarks > BL_LANDMARKS_BEST)
+    return set_err(BL_ERR_INVALID, "with_landmarks must be 0, BL_LANDMARKS_ALL or BL_LANDMARKS_BEST");
   if (frame_stride == 0) frame_stride = pitch * h;
   TRY(check_frames(frames, pixel_type, n, w, h, pitch, frame_stride));
   if (n < 1) return set_err(BL_ERR_INVALID, "empty batch");
@@ -1486,7 +1510,7 @@ int bl_submit(bl_ctx* c, const void* frames, int pixel_type, int n, int w, int h
   }
   c->plan = &c->plans[lane];
   c->st = lane ? c->lanes[lane] : c->user;
-  const int rc = enqueue(c, s, frames, pixel_type, n, w, h, pitch, frame_stride, with_landmarks != 0);
+  const int rc = enqueue(c, s, frames, pixel_type, n, w, h, pitch, frame_stride, with_landmarks);
   c->plan = &c->plans[0];
   c->st = c->user;
   TRY(rc);

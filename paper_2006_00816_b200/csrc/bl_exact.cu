@@ -579,7 +579,8 @@ __global__ void __launch_bounds__(1024) k_flatten(const DevDet* __restrict__ kep
                                                   int n_frames, int* __restrict__ offsets,
                                                   DevDet* __restrict__ flat, int* __restrict__ face_frame,
                                                   int* __restrict__ meta, long long flat_cap,
-                                                  const int* __restrict__ raw_overflow) {
+                                                  const int* __restrict__ raw_overflow, DevDet* __restrict__ best,
+                                                  int* __restrict__ best_frame) {
   // meta: [0, n) kept count per frame, [n] total kept, [n+1] raw-detection overflow flag
   __shared__ int s_part[1024];
   const int tid = threadIdx.x;
@@ -606,6 +607,23 @@ __global__ void __launch_bounds__(1024) k_flatten(const DevDet* __restrict__ kep
     offsets[n_frames] = s_part[tid];
     meta[n_frames] = s_part[tid];
     meta[n_frames + 1] = *raw_overflow;
+    meta[n_frames + 3] = n_frames;  // faces of the best-detection landmark list
+  }
+  if (best) {  // the face of every frame = its first kept detection (pipeline.cpp:167); a frame
+               // without one gets a placeholder box whose landmarks nobody reads
+    for (int f = tid; f < n_frames; f += blockDim.x) {
+      DevDet d;
+      if (kept_count[f] > 0) {
+        d = kept[(long long)f * cap_pf];
+      } else {
+        d.x = d.y = 0;
+        d.w = d.h = 1;
+        d.score = 0.0;
+        d.scale_index = d.rotation_index = 0;
+      }
+      best[f] = d;
+      best_frame[f] = f;
+    }
   }
   __syncthreads();
   // copy: warp per frame
@@ -624,9 +642,9 @@ __global__ void __launch_bounds__(1024) k_flatten(const DevDet* __restrict__ kep
 
 void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, long long cap_pf,
                     int n_frames, int* offsets, DevDet* flat, int* face_frame, int* meta,
-                    long long flat_cap, const int* raw_overflow) {
+                    long long flat_cap, const int* raw_overflow, DevDet* best, int* best_frame) {
   k_flatten<<<1, 1024, 0, L.st>>>(kept, kept_count, cap_pf, n_frames, offsets, flat, face_frame, meta,
-                                  flat_cap, raw_overflow);
+                                  flat_cap, raw_overflow, best, best_frame);
   ++*L.counter;
 }
 

@@ -251,7 +251,7 @@ void launch_nms(const Launch& L, const DevDet* dets, const int* det_count, long 
                 double iou_thr, DevDet* kept_out, int* kept_count, void* gkeys, long long gkeys_pf);
 void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, long long cap_pf,
                     int n_frames, int* offsets, DevDet* flat, int* face_frame, int* meta,
-                    long long flat_cap, const int* raw_overflow);
+                    long long flat_cap, const int* raw_overflow, DevDet* best = nullptr, int* best_frame = nullptr);
 // bl_ert.cu
 void launch_ert_init(const Launch& L, const ErtDev& M, const int* n_faces, int cap, double* cur);
 void launch_ert_level(const Launch& L, const ErtDev& M, int t, const void* frames, int u8, int w, int h,

@@ -12,6 +12,8 @@
 // identical results, like the reference's modes (acceptance C8).
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -142,79 +144,149 @@ int bl_run(bl_ctx* ctx, const char* frames_dir, double fps, int batch_size, bl_f
                                                        " < " + std::to_string(n) + " frames");
   const size_t fpx = (size_t)w * h;
   const int B = (int)std::min<int64_t>(batch_size, n);
-  std::vector<uint8_t> buf[2] = {std::vector<uint8_t>(fpx * B), std::vector<uint8_t>(fpx * B)};
-  std::vector<double> dec_ms(n, 0.0);
+  const int64_t n_batches = (n + B - 1) / B;
 
-  // decode batch b into buf[b & 1] (the next batch decodes on a helper thread while the
-  // device works on the current one)
-  auto decode = [&](int64_t b0, int nb, std::vector<uint8_t>& dst) -> int {
-    for (int i = 0; i < nb; ++i) {
-      const auto t0 = Clock::now();
-      int fw = 0, fh = 0;
-      if (int rc = bl_read_pgm(paths[b0 + i].c_str(), &fw, &fh, dst.data() + fpx * i, fpx)) return rc;
-      dec_ms[b0 + i] = ms_since(t0);
-    }
-    return BL_OK;
+  // Decode ring: kDecoders persistent decoder threads (batch b on thread b % kDecoders) parse
+  // PGMs straight to u8 into pinned buffer b % kRing while the device works on up to
+  // BL_MAX_IN_FLIGHT earlier batches (one upload per batch; detection and the best face's
+  // landmarks run in the same device pass).
+  const int kDecoders = (int)std::max<unsigned>(1u, std::min<unsigned>(4u, std::thread::hardware_concurrency() / 2));
+  const int kRing = BL_MAX_IN_FLIGHT + kDecoders;
+  struct RingBuf {
+    uint8_t* p = nullptr;
+    int64_t batch = -1;  // batch decoded into it (ready), -1: free
+    int rc = BL_OK;
+    std::string err;
   };
-  int rc = decode(0, B, buf[0]);
-  if (rc) return rc;
+  std::vector<RingBuf> ring(kRing);
+  for (RingBuf& r : ring)
+    if (int rc = bl_host_alloc(fpx * B, reinterpret_cast<void**>(&r.p))) {
+      for (RingBuf& q : ring) bl_host_free(q.p);
+      return rc;
+    }
+  std::vector<double> dec_ms(n, 0.0);
+  std::mutex mu;
+  std::condition_variable cv;
+  bool stop = false;
+  auto decode_loop = [&](int who) {
+    for (int64_t b = who; b < n_batches; b += kDecoders) {
+      RingBuf& r = ring[b % kRing];
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return stop || r.batch < 0; });
+        if (stop) return;
+      }
+      const int64_t b0 = b * B;
+      const int nb = (int)std::min<int64_t>(B, n - b0);
+      int rc = BL_OK;
+      for (int i = 0; i < nb && rc == BL_OK; ++i) {
+        const auto t0 = Clock::now();
+        int fw = 0, fh = 0;
+        rc = bl_read_pgm(paths[b0 + i].c_str(), &fw, &fh, r.p + fpx * i, fpx);
+        dec_ms[b0 + i] = ms_since(t0);
+      }
+      std::lock_guard<std::mutex> lk(mu);
+      r.rc = rc;
+      if (rc) r.err = bl_last_error();
+      r.batch = b;
+      cv.notify_all();
+      if (rc) return;
+    }
+  };
+  std::vector<std::thread> decoders;
+  for (int d = 0; d < kDecoders; ++d) decoders.emplace_back(decode_loop, d);
+  auto finish = [&](int rc) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+      cv.notify_all();
+    }
+    for (std::thread& t : decoders) t.join();
+    for (RingBuf& r : ring) bl_host_free(r.p);
+    return rc;
+  };
+
+  struct Pending {
+    uint64_t ticket;
+    int64_t b;
+    Clock::time_point t0;
+  };
+  std::vector<Pending> q;
+  std::vector<int32_t> counts(B);
+  std::vector<double> xy((size_t)B * 2 * L);
   int64_t total = 0;
-  std::vector<int32_t> counts(B), face_frame;
-  std::vector<bl_box> boxes;
-  std::vector<double> xy;
-  for (int64_t b0 = 0, bi = 0; b0 < n; b0 += B, ++bi) {
+  // results of batch p, in frame order (detect_frame + landmark_frame, pipeline.cpp:159-190)
+  auto collect_one = [&](const Pending& p) -> int {
+    const int64_t b0 = p.b * B;
     const int nb = (int)std::min<int64_t>(B, n - b0);
-    std::vector<uint8_t>& cur = buf[bi & 1];
-    const int64_t nb_next = std::min<int64_t>(B, n - (b0 + nb));
-    int rc_next = BL_OK;
-    std::thread next;
-    if (nb_next > 0) next = std::thread([&] { rc_next = decode(b0 + nb, (int)nb_next, buf[(bi + 1) & 1]); });
-    // detect (detect_frame, pipeline.cpp:159-169) for the batch, straight into the output
-    const auto td = Clock::now();
     int64_t got = 0;
-    rc = bl_detect(ctx, cur.data(), BL_PIX_U8, nb, w, h, (size_t)w, fpx, dets + total, det_cap - total, counts.data(),
-                   &got);
-    const double det_ms = ms_since(td);
-    // the face of each frame = its first detection; landmarks for the faces (pipeline.cpp:171-190)
-    face_frame.clear();
-    boxes.clear();
+    int rc = bl_collect(ctx, p.ticket, dets + total, det_cap - total, counts.data(), &got, xy.data());
+    const double batch_ms = ms_since(p.t0);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      ring[p.b % kRing].batch = -1;  // the decoder may refill it
+      cv.notify_all();
+    }
+    if (rc) return rc;
     int64_t off = total;
-    for (int i = 0; rc == BL_OK && i < nb; ++i) {
+    for (int i = 0; i < nb && rc == BL_OK; ++i) {
       bl_frame_result& fr = frames[b0 + i];
       std::memset(&fr, 0, sizeof fr);
       fr.frame_index = (int32_t)(b0 + i);
       fr.n_detections = counts[i];
       fr.t = double(b0 + i) / fps;
       fr.decode_ms = dec_ms[b0 + i];
-      fr.detect_ms = det_ms / nb;
-      if (counts[i] > 0) {
+      fr.detect_ms = batch_ms / nb;  // submit -> results, detection + landmarks in one device pass
+      fr.landmark_ms = 0.0;
+      if (counts[i] > 0) {  // the face = the first (best) detection, pipeline.cpp:167
         fr.face_found = 1;
         fr.face = dets[off];
-        face_frame.push_back(i);
-        boxes.push_back(dets[off].box);
+        const double* pxy = xy.data() + (size_t)i * 2 * L;
+        std::memcpy(landmarks + (b0 + i) * 2 * (int64_t)L, pxy, sizeof(double) * 2 * L);
+        rc = eye_ear(pxy, kLeft, fr.ear_left);
+        if (rc == BL_OK) rc = eye_ear(pxy, kRight, fr.ear_right);
       }
       off += counts[i];
     }
-    const auto tl = Clock::now();
-    if (rc == BL_OK && !boxes.empty()) {
-      xy.resize(boxes.size() * 2 * L);
-      rc = bl_landmarks(ctx, cur.data(), BL_PIX_U8, nb, w, h, (size_t)w, fpx, face_frame.data(), boxes.data(),
-                        (int64_t)boxes.size(), xy.data(), nullptr);
-    }
-    const double lm_ms = ms_since(tl);
-    for (size_t k = 0; rc == BL_OK && k < boxes.size(); ++k) {
-      bl_frame_result& fr = frames[b0 + face_frame[k]];
-      const double* p = xy.data() + k * 2 * L;
-      std::memcpy(landmarks + (b0 + face_frame[k]) * 2 * (int64_t)L, p, sizeof(double) * 2 * L);
-      rc = eye_ear(p, kLeft, fr.ear_left);
-      if (rc == BL_OK) rc = eye_ear(p, kRight, fr.ear_right);
-    }
-    for (int i = 0; i < nb; ++i) frames[b0 + i].landmark_ms = lm_ms / nb;
-    if (next.joinable()) next.join();
-    if (rc) return rc;
-    if (rc_next) return rc_next;
     total = off;
+    return rc;
+  };
+  int rc = BL_OK;
+  for (int64_t b = 0; b < n_batches && rc == BL_OK; ++b) {
+    RingBuf& r = ring[b % kRing];
+    {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return r.batch == b; });
+      if (r.rc) {
+        blb::set_last_error(r.err.c_str());
+        rc = r.rc;
+        break;
+      }
+    }
+    if ((int)q.size() == BL_MAX_IN_FLIGHT) {
+      rc = collect_one(q.front());
+      q.erase(q.begin());
+      if (rc) break;
+    }
+    const int nb = (int)std::min<int64_t>(B, n - b * B);
+    uint64_t t = 0;
+    const auto t0 = Clock::now();
+    rc = bl_submit(ctx, r.p, BL_PIX_U8, nb, w, h, (size_t)w, fpx, BL_LANDMARKS_BEST, &t);
+    if (rc == BL_OK) q.push_back({t, b, t0});
   }
+  while (!q.empty()) {  // drain (after an error: collect and discard, keeping the first error)
+    if (rc == BL_OK) {
+      rc = collect_one(q.front());
+    } else {
+      const std::string keep = bl_last_error();
+      int64_t got = 0;
+      bl_collect(ctx, q.front().ticket, dets + total, det_cap - total, counts.data(), &got, xy.data());
+      blb::set_last_error(keep.c_str());
+    }
+    q.erase(q.begin());
+  }
+  rc = finish(rc);
+  if (rc) return rc;
   *det_total = total;
   // build_trace (blink.cpp:47-93): per-eye baseline quantile over frames with a face
   if (fps <= 0.0) return fail(BL_ERR_INVALID, "build_trace: fps must be positive");

@@ -11,4 +11,5 @@ print("   ", {k: v["ms"] for k, v in c["C1"]["stages_ms"].items()})
 for k in ("C2", "C3", "C5"):
     print(k, c[k]["value"], "e2e", c[k]["e2e"]["value"], {s: v["ms"] for s, v in c[k]["stages_ms"].items()})
 print("C4", c["C4"]["value"])
+print("run", c["run"])
 PY
