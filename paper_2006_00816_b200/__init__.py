@@ -104,6 +104,8 @@ _SIGS = {
     "bl_collect": (C.c_int, [_vp, _u64, _vp, _i64, _vp, _P(_i64), _vp]),
     "bl_ctx_set_face_capacity": (C.c_int, [_vp, C.c_int]),
     "bl_ctx_get_face_capacity": (C.c_int, [_vp, _P(C.c_int)]),
+    "bl_host_alloc": (C.c_int, [_sz, _P(_vp)]),
+    "bl_host_free": (None, [_vp]),
     "bl_multi_create": (C.c_int, [_vp, C.c_int, _P(_vp)]),
     "bl_multi_destroy": (None, [_vp]),
     "bl_multi_size": (C.c_int, [_vp, _P(C.c_int)]),
