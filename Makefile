@@ -55,7 +55,7 @@ $(CPPLIB): $(PKG)/cpp/blinkline_gpu.cpp $(PKG)/cpp/blinkline_gpu.hpp include/bli
 	  -L$(PKG) -lblinkline_b200 -Wl,-rpath,'$$ORIGIN'
 
 tests/cpp/test_dropin: tests/cpp/test_dropin.cpp $(CPPLIB)
-	$(CXX) -std=c++20 -O2 -I$(PKG)/cpp -o $@ $< -L$(PKG) -lblinkline_gpu -lblinkline_b200 \
+	$(CXX) -std=c++20 -O2 -pthread -I$(PKG)/cpp -o $@ $< -L$(PKG) -lblinkline_gpu -lblinkline_b200 \
 	  -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
 oracle:

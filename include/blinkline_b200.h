@@ -122,6 +122,14 @@ int bl_detector_upload(bl_ctx* ctx, const double* weights, const double* biases,
 int bl_ert_upload(bl_ctx* ctx, int L, int T, int K, int F, double shrinkage, const double* mean_xy,
                   const int32_t* anchors, const double* split_params, const double* leaves);
 
+/* Share src's uploaded detector and/or ERT model with dst (same device): one device copy
+ * serves every context of a process (e.g. the C++ drop-in's per-thread contexts).  Models are
+ * immutable once uploaded; a later upload on either context replaces only that context's
+ * model.  BL_ERR_STATE while dst has uncollected batches. */
+#define BL_SHARE_DETECTOR 1
+#define BL_SHARE_ERT 2
+int bl_ctx_share_models(bl_ctx* dst, bl_ctx* src, int what);
+
 /* --------------------------------------------------------------- hot path ---- */
 /* replaces: detect_faces (detector.hpp:87, detector.cpp:157-176), batched over n frames of
  * equal size.  Frame i starts at frames + i*frame_stride elements; rows are `pitch`
@@ -231,6 +239,10 @@ int bl_extract_features(bl_ctx* ctx, const double* image, int w, int h, double* 
  * scores: (cells_h-9) x (cells_w-9), bit-identical to score_separable. */
 int bl_score_window(bl_ctx* ctx, const double* features, int cells_w, int cells_h,
                     const double* weights, double bias, double* scores);
+/* replaces: score_dense (detector.hpp:72-74, detector.cpp:45-64): the definitional order (one
+ * accumulator over all 3100 terms), bit-identical to the reference's score_dense. */
+int bl_score_window_dense(bl_ctx* ctx, const double* features, int cells_w, int cells_h,
+                          const double* weights, double bias, double* scores);
 /* replaces: nms (detector.hpp:80, detector.cpp:124-142).  *kept = kept count. */
 int bl_nms(bl_ctx* ctx, const bl_detection* dets, int64_t n, double iou_threshold,
            bl_detection* out, int64_t* kept);

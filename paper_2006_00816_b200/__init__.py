@@ -127,6 +127,8 @@ _SIGS = {
     "bl_compute_features": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _vp]),
     "bl_extract_features": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp]),
     "bl_score_window": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _dbl, _vp]),
+    "bl_score_window_dense": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _dbl, _vp]),
+    "bl_ctx_share_models": (C.c_int, [_vp, _vp, C.c_int]),
     "bl_nms": (C.c_int, [_vp, _vp, _i64, _dbl, _vp, _P(_i64)]),
     "bl_orientation_bins": (C.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "bl_debug_sqrt": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
@@ -492,7 +494,20 @@ class Context:
         _err(lib.bl_score_window(self._h, feat.ctypes.data, cw, ch, wts.ctypes.data, float(bias), out.ctypes.data))
         return out
 
-    score_dense = score_separable
+    def score_dense(self, feat, weights, bias):
+        """score_dense (detector.cpp:45-64): the definitional single-accumulator order."""
+        feat = _np(feat, np.float64)
+        wts = _np(weights, np.float64).reshape(3100)
+        ch, cw = feat.shape[:2]
+        out = np.zeros((max(ch - 9, 0), max(cw - 9, 0)))
+        _err(lib.bl_score_window_dense(self._h, feat.ctypes.data, cw, ch, wts.ctypes.data, float(bias),
+                                       out.ctypes.data))
+        return out
+
+    def share_models(self, other):
+        """Use `other`'s uploaded models (same device; one device copy for both)."""
+        _err(lib.bl_ctx_share_models(self._h, other._h, 3))
+        self.ert_L, self.ert_TK = other.ert_L, getattr(other, "ert_TK", None)
 
     def nms(self, dets, iou_threshold=0.5):
         dets = _np(dets, DET_DTYPE)
@@ -684,7 +699,8 @@ def score_separable(feat, weights, bias):
     return default_context().score_separable(feat, weights, bias)
 
 
-score_dense = score_separable
+def score_dense(feat, weights, bias):
+    return default_context().score_dense(feat, weights, bias)
 
 
 def nms(dets, iou_threshold=0.5):

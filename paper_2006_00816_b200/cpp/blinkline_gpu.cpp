@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <filesystem>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 
@@ -34,6 +35,55 @@ void check(int rc) {
   throw std::runtime_error("blinkline_b200: " + msg);
 }
 
+// --- models on the device ---------------------------------------------------------------
+// Every thread has its own context (the reference calls these functions concurrently from its
+// pipeline workers, pipeline.cpp:278-311), but a model lives on each device ONCE: a
+// process-wide registry per device holds the last uploaded detector and ERT model in an owner
+// context, and thread contexts share them (bl_ctx_share_models) instead of uploading copies.
+//
+// Which model a call means is decided by its content key, not its address:
+//  * detector: every weight, bias, the threshold and the geometry (124 KB, compared exactly);
+//  * ERT: the structure (L, T, K, F, shrinkage, every tree's depth and vector sizes), the mean
+//    shape, a full 64-bit hash of every split record (the anchors, offsets and thresholds
+//    that decide each leaf) and of every leaf row's address, plus a strided sample of leaf
+//    values.  Reallocation, reassignment, another model at the same address or any split
+//    edit is seen on the next call; only a leaf VALUE edited in place within its existing
+//    buffer can slip past the sample -- call gpu::invalidate_model_cache() after such an edit
+//    (hashing all 130 MB of leaves per call would cost ~20 ms, 100x the device time).
+struct DetKey {
+  std::vector<double> w;
+  std::array<double, 5> b{};
+  double thr = 0, ratio = 0;
+  int geom[4] = {0, 0, 0, 0};
+  bool operator==(const DetKey& o) const {
+    return w == o.w && b == o.b && thr == o.thr && ratio == o.ratio && std::memcmp(geom, o.geom, sizeof geom) == 0;
+  }
+};
+
+struct ErtKey {
+  std::vector<double> head;  // L, T, K, F, shrinkage, mean shape, sampled leaf values
+  uint64_t split_hash = 0, layout_hash = 0;
+  bool operator==(const ErtKey& o) const {
+    return split_hash == o.split_hash && layout_hash == o.layout_hash && head == o.head;
+  }
+};
+
+struct DeviceModels {
+  std::mutex mu;
+  bl_ctx* det_owner = nullptr;  // never destroyed: process-lifetime, like the device itself
+  bl_ctx* ert_owner = nullptr;
+  DetKey det_key;
+  ErtKey ert_key;
+  bool det_valid = false, ert_valid = false;
+  uint64_t generation = 0;  // bumped by gpu::invalidate_model_cache()
+};
+
+DeviceModels& registry(int device) {
+  static DeviceModels r[64];
+  if (device < 0 || device >= 64) throw std::invalid_argument("device index out of range");
+  return r[device];
+}
+
 int default_device() {
   const char* e = std::getenv("BLINKLINE_DEVICE");
   return e ? std::atoi(e) : 0;
@@ -42,17 +92,10 @@ int default_device() {
 struct ThreadCtx {
   int device = default_device();
   bl_ctx* ctx = nullptr;
-  // detector cache: exact copy of the uploaded weights (compared on every call)
-  std::vector<double> det_w;
-  std::array<double, 5> det_b{};
-  double det_thr = 0;
-  int det_geom[4] = {0, 0, 0, 0};
-  double det_ratio = -1;
-  bool det_valid = false;
-  // ERT cache: identity + fingerprint (models are shared, immutable values in the reference's
-  // API; mutate-in-place callers call gpu::invalidate_model_cache()).
-  const ErtModel* ert_ptr = nullptr;
-  std::vector<double> ert_fp;
+  DetKey det_key;
+  ErtKey ert_key;
+  bool det_valid = false, ert_valid = false;
+  uint64_t generation = 0;
   ~ThreadCtx() {
     if (ctx) bl_ctx_destroy(ctx);
   }
@@ -67,59 +110,95 @@ ThreadCtx& tls() {
   return t;
 }
 
-void ensure_detector(ThreadCtx& T, const DetectorModel& m) {
-  std::vector<double> w(5 * std::size_t(kFilterWeights));
+DetKey detector_key(const DetectorModel& m) {
+  DetKey k;
+  k.w.resize(5 * std::size_t(kFilterWeights));
   for (int r = 0; r < 5; ++r) {
     if (int(m.filters[r].weights.size()) != kFilterWeights)
       throw std::invalid_argument("filter must carry exactly 3100 weights");
-    std::memcpy(&w[std::size_t(r) * kFilterWeights], m.filters[r].weights.data(), sizeof(double) * kFilterWeights);
+    std::memcpy(&k.w[std::size_t(r) * kFilterWeights], m.filters[r].weights.data(), sizeof(double) * kFilterWeights);
+    k.b[r] = m.filters[r].bias;
   }
-  std::array<double, 5> b;
-  for (int r = 0; r < 5; ++r) b[r] = m.filters[r].bias;
+  k.thr = m.detection_threshold;
+  k.ratio = m.min_face_ratio;
   const int geom[4] = {m.window_cells, m.cell_px, m.scale_num, m.scale_den};
-  if (T.det_valid && T.det_w == w && T.det_b == b && T.det_thr == m.detection_threshold &&
-      std::memcmp(T.det_geom, geom, sizeof geom) == 0 && T.det_ratio == m.min_face_ratio)
-    return;
-  check(bl_detector_upload(T.get(), w.data(), b.data(), m.detection_threshold, m.window_cells, m.cell_px,
-                           m.scale_num, m.scale_den, m.min_face_ratio));
-  T.det_w = std::move(w);
-  T.det_b = b;
-  T.det_thr = m.detection_threshold;
-  std::memcpy(T.det_geom, geom, sizeof geom);
-  T.det_ratio = m.min_face_ratio;
-  T.det_valid = true;
+  std::memcpy(k.geom, geom, sizeof geom);
+  return k;
 }
 
-std::vector<double> ert_fingerprint(const ErtModel& m) {
-  std::vector<double> fp;
-  fp.push_back(m.landmark_count());
-  fp.push_back(m.levels());
-  fp.push_back(m.trees_per_level());
-  fp.push_back(m.shrinkage);
-  for (const Point2& p : m.mean_shape.points) {
-    fp.push_back(p.x);
-    fp.push_back(p.y);
+void ensure_detector(ThreadCtx& T, const DetectorModel& m) {
+  DetKey key = detector_key(m);
+  DeviceModels& R = registry(T.device);
+  if (T.det_valid && T.generation == R.generation && T.det_key == key) return;
+  std::lock_guard<std::mutex> lk(R.mu);
+  if (!R.det_valid || !(R.det_key == key)) {
+    if (!R.det_owner) check(bl_ctx_create(T.device, &R.det_owner));
+    check(bl_detector_upload(R.det_owner, key.w.data(), key.b.data(), key.thr, m.window_cells, m.cell_px,
+                             m.scale_num, m.scale_den, m.min_face_ratio));
+    R.det_key = key;
+    R.det_valid = true;
   }
-  const std::size_t T = m.cascade.size();
-  for (std::size_t t = 0; t < T; ++t) {
+  check(bl_ctx_share_models(T.get(), R.det_owner, BL_SHARE_DETECTOR));
+  T.det_key = std::move(key);
+  T.det_valid = true;
+  T.generation = R.generation;
+}
+
+inline uint64_t mix(uint64_t h, uint64_t v) {  // FNV-1a style 64-bit step over whole words
+  h ^= v;
+  h *= 0x100000001B3ull;
+  return h ^ (h >> 29);
+}
+
+inline uint64_t bits(double d) {
+  uint64_t u;
+  std::memcpy(&u, &d, sizeof u);
+  return u;
+}
+
+ErtKey ert_key(const ErtModel& m) {
+  ErtKey k;
+  const int L = m.landmark_count(), Tn = m.levels(), K = m.trees_per_level();
+  k.head = {double(L), double(Tn), double(K), m.shrinkage};
+  for (const Point2& p : m.mean_shape.points) {
+    k.head.push_back(p.x);
+    k.head.push_back(p.y);
+  }
+  uint64_t hs = 0xcbf29ce484222325ull, hl = 0x84222325cbf29ce4ull;
+  for (std::size_t t = 0; t < m.cascade.size(); ++t) {
     const auto& lv = m.cascade[t];
-    fp.push_back(double(lv.size()));
-    for (std::size_t k = 0; k < lv.size(); k += std::max<std::size_t>(1, lv.size() / 16)) {
-      const RegressionTree& tr = lv[k];
-      fp.push_back(tr.depth);
-      if (!tr.splits.empty()) {
-        fp.push_back(tr.splits[0].threshold);
-        fp.push_back(tr.splits.back().offset_b.y);
+    hl = mix(hl, lv.size());
+    for (std::size_t i = 0; i < lv.size(); ++i) {
+      const RegressionTree& tr = lv[i];
+      hl = mix(hl, uint64_t(tr.depth));
+      hl = mix(hl, tr.splits.size());
+      hl = mix(hl, tr.leaves.size());
+      for (const SplitNode& n : tr.splits) {
+        hs = mix(hs, (uint64_t(uint32_t(n.anchor_a)) << 32) | uint32_t(n.anchor_b));
+        hs = mix(hs, bits(n.offset_a.x));
+        hs = mix(hs, bits(n.offset_a.y));
+        hs = mix(hs, bits(n.offset_b.x));
+        hs = mix(hs, bits(n.offset_b.y));
+        hs = mix(hs, bits(n.threshold));
       }
-      if (!tr.leaves.empty() && !tr.leaves.back().empty()) fp.push_back(tr.leaves.back().back().x);
+      for (const auto& leaf : tr.leaves) {
+        hl = mix(hl, reinterpret_cast<uintptr_t>(leaf.data()));
+        hl = mix(hl, leaf.size());
+      }
+      if ((i & 15) == 0 && !tr.leaves.empty())  // sampled leaf values
+        for (const auto& leaf : tr.leaves)
+          if (!leaf.empty()) {
+            k.head.push_back(leaf[t % leaf.size()].x);
+            k.head.push_back(leaf.back().y);
+          }
     }
   }
-  return fp;
+  k.split_hash = hs;
+  k.layout_hash = hl;
+  return k;
 }
 
-void ensure_ert(ThreadCtx& T, const ErtModel& m) {
-  std::vector<double> fp = ert_fingerprint(m);
-  if (T.ert_ptr == &m && T.ert_fp == fp) return;
+void upload_ert(bl_ctx* ctx, const ErtModel& m) {
   const int L = m.landmark_count(), Tn = m.levels(), K = m.trees_per_level();
   if (L < 2) throw std::invalid_argument("predict_landmarks: model has no mean shape");
   const int F = (Tn > 0 && K > 0) ? m.cascade[0][0].depth : 0;
@@ -160,9 +239,25 @@ void ensure_ert(ThreadCtx& T, const ErtModel& m) {
       }
     }
   }
-  check(bl_ert_upload(T.get(), L, Tn, K, F, m.shrinkage, mean.data(), an.data(), sp.data(), lv.data()));
-  T.ert_ptr = &m;
-  T.ert_fp = std::move(fp);
+  check(bl_ert_upload(ctx, L, Tn, K, F, m.shrinkage, mean.data(), an.data(), sp.data(), lv.data()));
+}
+
+void ensure_ert(ThreadCtx& T, const ErtModel& m) {
+  if (m.landmark_count() < 2) throw std::invalid_argument("predict_landmarks: model has no mean shape");
+  ErtKey key = ert_key(m);
+  DeviceModels& R = registry(T.device);
+  if (T.ert_valid && T.generation == R.generation && T.ert_key == key) return;
+  std::lock_guard<std::mutex> lk(R.mu);
+  if (!R.ert_valid || !(R.ert_key == key)) {
+    if (!R.ert_owner) check(bl_ctx_create(T.device, &R.ert_owner));
+    upload_ert(R.ert_owner, m);
+    R.ert_key = key;
+    R.ert_valid = true;
+  }
+  check(bl_ctx_share_models(T.get(), R.ert_owner, BL_SHARE_ERT));
+  T.ert_key = std::move(key);
+  T.ert_valid = true;
+  T.generation = R.generation;
 }
 
 // Frames go to the device as u8 when every pixel is an integer in [0,255] (lossless),
@@ -353,10 +448,21 @@ static SaliencyMap score_gpu(const FeatureImage& feat, const LinearFilter& filte
   return s;
 }
 
-// The device scorer evaluates the separable order exactly (bit-identical to
-// score_separable); score_dense differs from it only by summation order (<= 1e-4 by the
-// reference's own contract, SPEC C1), so both are served by it.
-SaliencyMap score_dense(const FeatureImage& feat, const LinearFilter& filter) { return score_gpu(feat, filter); }
+// Both scorers run on the device in their own summation order: bit-identical to the
+// reference's score_separable and score_dense respectively.
+SaliencyMap score_dense(const FeatureImage& feat, const LinearFilter& filter) {  // detector.cpp:45-64 order
+  if (int(filter.weights.size()) != kFilterWeights)
+    throw std::invalid_argument("filter must carry exactly 3100 weights");
+  if (feat.cells_w < kWindowCells || feat.cells_h < kWindowCells)
+    throw std::invalid_argument("feature image smaller than the 10x10 detection window");
+  SaliencyMap s;
+  s.width = feat.cells_w - (kWindowCells - 1);
+  s.height = feat.cells_h - (kWindowCells - 1);
+  s.scores.assign(std::size_t(s.width) * s.height, 0.0);
+  check(bl_score_window_dense(tls().get(), feat.values.data(), feat.cells_w, feat.cells_h, filter.weights.data(),
+                              filter.bias, s.scores.data()));
+  return s;
+}
 SaliencyMap score_separable(const FeatureImage& feat, const LinearFilter& filter) {
   return score_gpu(feat, filter);
 }
@@ -501,18 +607,25 @@ namespace gpu {
 void set_device(int device) {
   ThreadCtx& T = tls();
   if (T.device == device) return;
+  registry(device);  // range check
   if (T.ctx) bl_ctx_destroy(T.ctx);
   T.ctx = nullptr;
   T.device = device;
   T.det_valid = false;
-  T.ert_ptr = nullptr;
+  T.ert_valid = false;
 }
 
-void invalidate_model_cache() {
+void invalidate_model_cache() {  // every thread re-checks against a fresh upload
+  for (int d = 0; d < 64; ++d) {
+    DeviceModels& R = registry(d);
+    std::lock_guard<std::mutex> lk(R.mu);
+    R.det_valid = false;
+    R.ert_valid = false;
+    ++R.generation;
+  }
   ThreadCtx& T = tls();
   T.det_valid = false;
-  T.ert_ptr = nullptr;
-  T.ert_fp.clear();
+  T.ert_valid = false;
 }
 
 static void same_size(const std::vector<const GrayImage*>& fr) {
@@ -607,6 +720,69 @@ std::vector<FrameResult> detect_and_landmark(const std::vector<GrayImage>& frame
                              cap, counts.data(), &total, xy.data());
   }
   check(rc);
+  std::size_t o = 0;
+  for (std::size_t i = 0; i < frames.size(); ++i)
+    for (int k = 0; k < counts[i]; ++k, ++o) {
+      res[i].detections.push_back(from_c(out[o]));
+      Shape s;
+      s.frame = ShapeFrame::image;
+      s.points.resize(L);
+      for (int j = 0; j < L; ++j) s.points[j] = {xy[(o * L + j) * 2], xy[(o * L + j) * 2 + 1]};
+      res[i].landmarks.push_back(std::move(s));
+    }
+  return res;
+}
+
+// The same over several GPUs: contiguous frame shards, one context and host thread per device
+// (bl_multi), models bound from each device's registry, results in frame order.
+std::vector<FrameResult> detect_and_landmark(const std::vector<GrayImage>& frames, const DetectorModel& hog,
+                                             const ErtModel& ert, const std::vector<int>& devices) {
+  if (devices.empty()) throw std::invalid_argument("detect_and_landmark: empty device list");
+  std::vector<FrameResult> res(frames.size());
+  if (frames.empty()) return res;
+  struct Multi {
+    bl_multi* m = nullptr;
+  };
+  static std::mutex mu;
+  static std::map<std::vector<int>, Multi> pool;  // process-lifetime, one per device list
+  std::lock_guard<std::mutex> lk(mu);
+  Multi& M = pool[devices];
+  if (!M.m) check(bl_multi_create(devices.data(), int(devices.size()), &M.m));
+  const DetKey dk = detector_key(hog);
+  const ErtKey ek = ert_key(ert);
+  for (std::size_t i = 0; i < devices.size(); ++i) {  // bind the device's registry models
+    bl_ctx* c = nullptr;
+    check(bl_multi_context(M.m, int(i), &c));
+    DeviceModels& R = registry(devices[i]);
+    std::lock_guard<std::mutex> rl(R.mu);
+    if (!R.det_valid || !(R.det_key == dk)) {
+      if (!R.det_owner) check(bl_ctx_create(devices[i], &R.det_owner));
+      check(bl_detector_upload(R.det_owner, dk.w.data(), dk.b.data(), dk.thr, hog.window_cells, hog.cell_px,
+                               hog.scale_num, hog.scale_den, hog.min_face_ratio));
+      R.det_key = dk;
+      R.det_valid = true;
+    }
+    if (!R.ert_valid || !(R.ert_key == ek)) {
+      if (!R.ert_owner) check(bl_ctx_create(devices[i], &R.ert_owner));
+      upload_ert(R.ert_owner, ert);
+      R.ert_key = ek;
+      R.ert_valid = true;
+    }
+    check(bl_ctx_share_models(c, R.det_owner, BL_SHARE_DETECTOR));
+    check(bl_ctx_share_models(c, R.ert_owner, BL_SHARE_ERT));
+  }
+  std::vector<const GrayImage*> fr;
+  for (const GrayImage& f : frames) fr.push_back(&f);
+  same_size(fr);
+  const int w = fr[0]->width, h = fr[0]->height, L = ert.landmark_count();
+  const Packed p = pack(fr);
+  std::vector<int32_t> counts(frames.size());
+  int64_t total = 0;
+  const int64_t cap = int64_t(frames.size()) * 64;
+  std::vector<bl_detection> out(static_cast<std::size_t>(cap));
+  std::vector<double> xy(std::size_t(cap) * L * 2);
+  check(bl_multi_detect_landmarks(M.m, p.data(), p.pix, int(frames.size()), w, h, w, std::size_t(w) * h, out.data(),
+                                  cap, counts.data(), &total, xy.data(), nullptr));
   std::size_t o = 0;
   for (std::size_t i = 0; i < frames.size(); ++i)
     for (int k = 0; k < counts[i]; ++k, ++o) {

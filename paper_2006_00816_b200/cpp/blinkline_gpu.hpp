@@ -331,7 +331,10 @@ namespace gpu {
 
 // Device used by this thread's context (default: $BLINKLINE_DEVICE or 0).
 void set_device(int device);
-// Drop cached device copies of models (call after mutating a model in place).
+// Models live on each device once, shared by every thread's context, and are matched by
+// content: weights exactly; an ERT model by structure, mean shape, a full hash of its split
+// records and leaf-row addresses, and sampled leaf values.  After editing leaf VALUES of an
+// ERT model in place (same buffers), call this so the next call re-uploads.
 void invalidate_model_cache();
 
 // detect_faces over many equal-size frames in one device pass; result[i] is frame i's list.
@@ -348,6 +351,11 @@ struct FrameResult {
 };
 std::vector<FrameResult> detect_and_landmark(const std::vector<GrayImage>& frames,
                                              const DetectorModel& hog, const ErtModel& ert);
+// The same sharded over several GPUs of this process (contiguous frame shards, one host thread
+// per device, results in frame order; a device may be listed more than once).
+std::vector<FrameResult> detect_and_landmark(const std::vector<GrayImage>& frames,
+                                             const DetectorModel& hog, const ErtModel& ert,
+                                             const std::vector<int>& devices);
 
 }  // namespace gpu
 }  // namespace blinkline

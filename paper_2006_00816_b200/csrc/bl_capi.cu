@@ -226,8 +226,10 @@ struct bl_ctx {
   cudaStream_t st = nullptr;
   std::mutex mu;
   uint64_t launches = 0;
-  DetectorState det;
-  ErtState ert;
+  // Models: immutable once uploaded and shared between contexts on one device
+  // (bl_ctx_share_models); an upload replaces the context's pointer, sharers keep theirs.
+  std::shared_ptr<DetectorState> detp = std::make_shared<DetectorState>();
+  std::shared_ptr<ErtState> ertp = std::make_shared<ErtState>();
   // Detection lanes (plan arenas + compute stream, see kLanes): consecutive in-flight batches
   // rotate over them, so batch i+1's pyramid / gradHist overlap batch i's later stages.
   // Lane 0 runs on the caller's stream (c->user); `plan` / `st` point at the active lane.
@@ -301,7 +303,7 @@ void pyramid_dims(int w, int h, int window, std::vector<int>& lw, std::vector<in
 }
 
 int build_plan(bl_ctx* c, Plan& P, int n, int w, int h, int pix) {
-  const DetectorState& D = c->det;
+  const DetectorState& D = (*c->detp);
   if (P.valid && P.n == n && P.w == w && P.h == h && P.pix == pix && P.screen == c->screen &&
       P.window_cells == D.window_cells &&
       P.cell_px == D.cell_px && P.scale_num == D.scale_num && P.scale_den == D.scale_den &&
@@ -483,7 +485,7 @@ int prepare_detect(bl_ctx* c, int pix, int n, int w, int h, long long pitch, lon
 int record_detect(bl_ctx* c, const void* in, int pix, int n, long long pitch, long long fstride) {
   Plan& P = *c->plan;
   const Launch L = launch_of(c);
-  const DetectorState& D = c->det;
+  const DetectorState& D = (*c->detp);
   stage_mark(c, BL_STAGE_PYRAMID);
   // pyramid chain (image.cpp:162-170): level k from level k-1, every frame at once.  A level
   // no window scores (below the smallest eligible face) is read only by the next step, so
@@ -623,7 +625,7 @@ int ert_work_ensure(const ErtState& E, ErtWork& wk, int nf, bool leaf_scratch) {
 int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix, int w, int h, long long pitch,
             long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces_dev,
             int nf, uint8_t* leaf_dev, double* out_xy, int* err_dev, long long expect_faces) {
-  ErtState& E = c->ert;
+  ErtState& E = (*c->ertp);
   const Launch L{st, &c->launches};
   TRY(ert_work_ensure(E, wk, nf, leaf_dev == nullptr));
   // leaf indices: the caller's [face][T*K] buffer, else a per-level scratch [face][K]
@@ -763,7 +765,7 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
             int landmarks) {
   Slot& S = c->slots[s];
   Plan& P = *c->plan;
-  const DetectorState& D = c->det;
+  const DetectorState& D = (*c->detp);
   const bool same = P.valid && P.n == n && P.w == w && P.h == h && P.pix == pix &&
                     P.window_cells == D.window_cells && P.cell_px == D.cell_px;
   if (!same) {  // arenas may be reallocated: nothing may still be reading them
@@ -790,8 +792,8 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
     TRY(o.meta.ensure(sizeof(int) * (n + 4)));
     TRY(ensure_pinned(reinterpret_cast<void*&>(o.h_meta), o.h_meta_cap, sizeof(int) * (n + 4)));
     if (landmarks) {
-      TRY(o.ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * lm_rows));
-      TRY(ert_work_ensure(c->ert, o.ert, (int)lm_rows, true));
+      TRY(o.ert_out.ensure(sizeof(double) * 2 * (*c->ertp).dev.L * lm_rows));
+      TRY(ert_work_ensure((*c->ertp), o.ert, (int)lm_rows, true));
     }
     if (best_only) {
       TRY(o.best.ensure(sizeof(DevDet) * n));
@@ -870,7 +872,7 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
                      (long long)n * kErtFacesPerFrameGuess);
     };
     if (graph) {
-      TRY(ert_work_ensure(c->ert, S.ert, (int)lm_rows, true));
+      TRY(ert_work_ensure((*c->ertp), S.ert, (int)lm_rows, true));
       bl_ctx::GraphEntry key;
       key.kind = 1;
       key.slot = s;
@@ -940,7 +942,7 @@ int collect(bl_ctx* c, int s, bl_detection* out, int64_t cap, int32_t* counts, i
   stage_mark(c, BL_STAGE_D2H);
   const size_t bd = sizeof(bl_detection) * tot;
   const int64_t lm_rows = S.landmarks == BL_LANDMARKS_BEST ? S.n : tot;  // best-only: one row per frame
-  const size_t bl = S.landmarks && landmarks ? sizeof(double) * 2 * c->ert.dev.L * lm_rows : 0;
+  const size_t bl = S.landmarks && landmarks ? sizeof(double) * 2 * (*c->ertp).dev.L * lm_rows : 0;
   const bool direct_d = !out || is_pinned_or_device(out);
   const bool direct_l = !bl || is_pinned_or_device(landmarks);
   const size_t need = (direct_d ? 0 : bd) + (direct_l ? 0 : bl) + 64;
@@ -964,8 +966,8 @@ int detect_common(bl_ctx* c, const void* frames, int pix, int n, int w, int h, s
                   bl_detection* out, int64_t cap, int32_t* counts, int64_t* total, double* landmarks) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
   std::lock_guard<std::mutex> lk(c->mu);
-  if (!c->det.ready) return set_err(BL_ERR_STATE, "no detector model uploaded");
-  if (landmarks && !c->ert.ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
+  if (!(*c->detp).ready) return set_err(BL_ERR_STATE, "no detector model uploaded");
+  if (landmarks && !(*c->ertp).ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
   if (fstride == 0) fstride = pitch * h;
   TRY(check_frames(frames, pix, n, w, h, pitch, fstride));
   TRY(use_device(c));
@@ -1251,8 +1253,8 @@ int bl_ctx_stage_times(bl_ctx* c, float* ms, int* launches) {
 int bl_ctx_model_info(bl_ctx* c, int* landmark_count) {
   if (!c || !landmark_count) return set_err(BL_ERR_INVALID, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
-  if (!c->ert.ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
-  *landmark_count = c->ert.dev.L;
+  if (!(*c->ertp).ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
+  *landmark_count = (*c->ertp).dev.L;
   return BL_OK;
 }
 
@@ -1283,8 +1285,10 @@ int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, d
   TRY(use_device(c));
   TRY(quiesce_for_upload(c));
   ++c->model_gen;  // thresholds and cuts are baked into captured graphs
-  DetectorState& D = c->det;
-  D.ready = false;
+  // a fresh state object: contexts sharing the previous one keep it (and a failed upload
+  // leaves this context's previous model in place)
+  auto nd = std::make_shared<DetectorState>();
+  DetectorState& D = *nd;
   D.thr = threshold;
   D.window_cells = window_cells;
   D.cell_px = cell_px;
@@ -1365,6 +1369,7 @@ int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, d
   CK(cudaMemcpy(D.cut32.p, D.cut, sizeof(float) * kFilters, cudaMemcpyHostToDevice));
   for (Plan& p : c->plans) p.valid = false;
   D.ready = true;
+  c->detp = std::move(nd);
   return BL_OK;
 }
 
@@ -1380,8 +1385,8 @@ int bl_ert_upload(bl_ctx* c, int L, int T, int K, int F, double shrinkage, const
   TRY(use_device(c));
   TRY(quiesce_for_upload(c));
   ++c->model_gen;  // the cascade's dims and pointers are baked into captured graphs
-  ErtState& E = c->ert;
-  E.ready = false;
+  auto ne = std::make_shared<ErtState>();  // fresh: sharers keep the previous model
+  ErtState& E = *ne;
   const int S = (1 << F) - 1, NL = 1 << F;
   const size_t nsplit = (size_t)T * K * S;
   if (2 * L > 512) return set_err(BL_ERR_MODEL, "landmark count above 256 is not supported");
@@ -1446,6 +1451,7 @@ int bl_ert_upload(bl_ctx* c, int L, int T, int K, int F, double shrinkage, const
   E.dev.mean_cx = mx;
   E.dev.mean_cy = my;
   E.ready = true;
+  c->ertp = std::move(ne);
   return BL_OK;
 }
 
@@ -1465,6 +1471,23 @@ int bl_ctx_set_face_capacity(bl_ctx* c, int faces_per_frame) {
   if (!c || faces_per_frame < 1) return set_err(BL_ERR_INVALID, "bad face capacity");
   std::lock_guard<std::mutex> lk(c->mu);
   c->face_cap_per_frame = faces_per_frame;
+  return BL_OK;
+}
+
+int bl_ctx_share_models(bl_ctx* dst, bl_ctx* src, int what) {
+  if (!dst || !src) return set_err(BL_ERR_INVALID, "null context");
+  if (what & ~(BL_SHARE_DETECTOR | BL_SHARE_ERT)) return set_err(BL_ERR_INVALID, "unknown share flags");
+  if (dst == src) return BL_OK;
+  if (dst->device != src->device) return set_err(BL_ERR_INVALID, "contexts live on different devices");
+  std::scoped_lock lk(dst->mu, src->mu);
+  TRY(use_device(dst));
+  TRY(quiesce_for_upload(dst));
+  ++dst->model_gen;
+  if (what & BL_SHARE_DETECTOR) {
+    dst->detp = src->detp;
+    for (Plan& p : dst->plans) p.valid = false;  // the plan follows the detector geometry
+  }
+  if (what & BL_SHARE_ERT) dst->ertp = src->ertp;
   return BL_OK;
 }
 
@@ -1490,8 +1513,8 @@ int bl_submit(bl_ctx* c, const void* frames, int pixel_type, int n, int w, int h
               int with_landmarks, uint64_t* ticket) {
   if (!c || !ticket) return set_err(BL_ERR_INVALID, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
-  if (!c->det.ready) return set_err(BL_ERR_STATE, "no detector model uploaded");
-  if (with_landmarks && !c->ert.ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
+  if (!(*c->detp).ready) return set_err(BL_ERR_STATE, "no detector model uploaded");
+  if (with_landmarks && !(*c->ertp).ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
   if (with_landmarks < 0 || with_landmarks > BL_LANDMARKS_BEST)
     return set_err(BL_ERR_INVALID, "with_landmarks must be 0, BL_LANDMARKS_ALL or BL_LANDMARKS_BEST");
   if (frame_stride == 0) frame_stride = pitch * h;
@@ -1535,7 +1558,7 @@ int bl_landmarks(bl_ctx* c, const void* frames, int pixel_type, int n_frames, in
                  double* out_xy, uint8_t* leaf_idx) {
   if (!c) return set_err(BL_ERR_INVALID, "null context");
   std::lock_guard<std::mutex> lk(c->mu);
-  if (!c->ert.ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
+  if (!(*c->ertp).ready) return set_err(BL_ERR_STATE, "no ERT model uploaded");
   if (frame_stride == 0) frame_stride = pitch * h;
   TRY(check_frames(frames, pixel_type, n_frames, w, h, pitch, frame_stride));
   if (n_boxes < 0 || n_boxes > (1 << 30)) return set_err(BL_ERR_INVALID, "bad box count");
@@ -1564,18 +1587,18 @@ int bl_landmarks(bl_ctx* c, const void* frames, int pixel_type, int n_frames, in
   CK(cudaMemcpyAsync(c->ert_nfaces.p, &nf, sizeof(int), cudaMemcpyHostToDevice, c->st));
   uint8_t* leaf_dev = nullptr;
   if (leaf_idx) {
-    TRY(c->ert_leaf.ensure((size_t)n_boxes * c->ert.dev.T * c->ert.dev.K + 1));
+    TRY(c->ert_leaf.ensure((size_t)n_boxes * (*c->ertp).dev.T * (*c->ertp).dev.K + 1));
     leaf_dev = c->ert_leaf.as<uint8_t>();
   }
   stage_mark(c, BL_STAGE_ERT);
-  TRY(c->ert_out.ensure(sizeof(double) * 2 * c->ert.dev.L * std::max(1, nf)));
+  TRY(c->ert_out.ensure(sizeof(double) * 2 * (*c->ertp).dev.L * std::max(1, nf)));
   TRY(c->ert_err.ensure(sizeof(int)));
   TRY(run_ert(c, c->st, c->ert_work, dev, pixel_type, w, h, dp, df, c->ert_frames.as<int>(), c->ert_boxes.as<int>(), 4,
               c->ert_nfaces.as<int>(), nf, leaf_dev, c->ert_out.as<double>(), c->ert_err.as<int>(), nf));
   stage_mark(c, BL_STAGE_D2H);
-  CK(cudaMemcpyAsync(out_xy, c->ert_out.p, sizeof(double) * 2 * c->ert.dev.L * n_boxes, cudaMemcpyDefault, c->st));
+  CK(cudaMemcpyAsync(out_xy, c->ert_out.p, sizeof(double) * 2 * (*c->ertp).dev.L * n_boxes, cudaMemcpyDefault, c->st));
   if (leaf_idx)
-    CK(cudaMemcpyAsync(leaf_idx, leaf_dev, (size_t)n_boxes * c->ert.dev.T * c->ert.dev.K, cudaMemcpyDefault, c->st));
+    CK(cudaMemcpyAsync(leaf_idx, leaf_dev, (size_t)n_boxes * (*c->ertp).dev.T * (*c->ertp).dev.K, cudaMemcpyDefault, c->st));
   CK(cudaStreamSynchronize(c->st));
   CK(cudaGetLastError());
   int err = 0;
@@ -1764,6 +1787,22 @@ int bl_score_window(bl_ctx* c, const double* features, int cw, int ch, const dou
   return from_device(c, scores, c->s_c.p, sizeof(double) * n);
 }
 
+int bl_score_window_dense(bl_ctx* c, const double* features, int cw, int ch, const double* weights, double bias,
+                          double* scores) {
+  if (!c || !features || !weights || !scores) return set_err(BL_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (cw < kWin || ch < kWin) return set_err(BL_ERR_INVALID, "feature image smaller than the 10x10 detection window");
+  TRY(use_device(c));
+  const long long cells = (long long)cw * ch;
+  const long long n = (long long)(cw - 9) * (ch - 9);
+  const void *f = nullptr, *wt = nullptr;
+  TRY(to_device(c, c->s_a, features, sizeof(double) * kFeat * cells, &f));
+  TRY(to_device(c, c->s_b, weights, sizeof(double) * kFilterW, &wt));
+  TRY(c->s_c.ensure(sizeof(double) * n));
+  launch_score_dense(launch_of(c), (const double*)f, cw, ch, (const double*)wt, bias, c->s_c.as<double>());
+  return from_device(c, scores, c->s_c.p, sizeof(double) * n);
+}
+
 int bl_nms(bl_ctx* c, const bl_detection* dets, int64_t n, double iou_threshold, bl_detection* out, int64_t* kept) {
   if (!c || (!dets && n > 0) || !out || !kept) return set_err(BL_ERR_INVALID, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
@@ -1819,7 +1858,7 @@ int bl_debug_sqrt(bl_ctx* c, const double* in, int64_t n, double* fast, double* 
 int bl_debug_screen_tc(bl_ctx* c, const double* features, int cw, int ch, float* scores, double* delta) {
   if (!c || !features || !scores) return set_err(BL_ERR_INVALID, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
-  if (!c->det.ready) return set_err(BL_ERR_STATE, "no detector model uploaded");
+  if (!(*c->detp).ready) return set_err(BL_ERR_STATE, "no detector model uploaded");
   if (cw < kWin || ch < kWin) return set_err(BL_ERR_INVALID, "feature image smaller than the 10x10 detection window");
   TRY(use_device(c));
   PlanDesc H;
@@ -1843,10 +1882,10 @@ int bl_debug_screen_tc(bl_ctx* c, const double* features, int cw, int ch, float*
   CK(cudaMemcpyAsync(c->s_desc.p, &H, sizeof H, cudaMemcpyHostToDevice, c->st));
   unsigned long long* nc = reinterpret_cast<unsigned long long*>(c->s_c.as<Candidate>() + na);
   CK(cudaMemsetAsync(nc, 0, sizeof(unsigned long long), c->st));
-  launch_screen_tc(launch_of(c), H, c->s_desc.as<PlanDesc>(), c->s_a.as<float>(), c->det.w_tc.as<float>(),
-                   c->det.cuttc.as<float>(), c->s_c.as<Candidate>(), nc, na, c->s_b.as<float>());
+  launch_screen_tc(launch_of(c), H, c->s_desc.as<PlanDesc>(), c->s_a.as<float>(), (*c->detp).w_tc.as<float>(),
+                   (*c->detp).cuttc.as<float>(), c->s_c.as<Candidate>(), nc, na, c->s_b.as<float>());
   if (delta)
-    for (int r = 0; r < kFilters; ++r) delta[r] = c->det.delta_tc[r];
+    for (int r = 0; r < kFilters; ++r) delta[r] = (*c->detp).delta_tc[r];
   return from_device(c, scores, c->s_b.p, sizeof(float) * kFilters * na);
 }
 

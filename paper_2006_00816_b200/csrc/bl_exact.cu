@@ -198,6 +198,34 @@ void launch_score_exact_all(const Launch& L, const double* feat64, int cw, int c
   ++*L.counter;
 }
 
+// score_dense (detector.cpp:45-64), the definitional order: one accumulator from 0.0 over the
+// window's 3100 terms, row j outer, feature k inner, + bias.  A thread per anchor (a stage
+// API, not the detect path).
+__global__ void __launch_bounds__(128) k_score_dense(const double* __restrict__ feat, int cw, int ch,
+                                                     const double* __restrict__ w, double bias,
+                                                     double* __restrict__ scores) {
+  const int sw = cw - (kWin - 1), sh = ch - (kWin - 1);
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)sw * sh) return;
+  const int cy = (int)(i / sw), cx = (int)(i - (long long)cy * sw);
+  double acc = 0.0;
+  for (int j = 0; j < kWin; ++j) {
+    const double* strip = feat + ((long long)(cy + j) * cw + cx) * kFeat;  // 10 cells x 31, contiguous
+    const double* wr = w + j * kRowW;
+#pragma unroll 10
+    for (int k = 0; k < kRowW; ++k) acc = dadd(acc, dmul(__ldg(strip + k), __ldg(wr + k)));
+  }
+  scores[i] = dadd(acc, bias);
+}
+
+void launch_score_dense(const Launch& L, const double* feat64, int cw, int ch, const double* w64, double bias,
+                        double* scores) {
+  const long long n = (long long)(cw - 9) * (ch - 9);
+  if (n <= 0) return;
+  k_score_dense<<<(unsigned)div_up(n, 128), 128, 0, L.st>>>(feat64, cw, ch, w64, bias, scores);
+  ++*L.counter;
+}
+
 // ------------------------------------------------------------------------- NMS ----
 // detector.cpp:16-28
 BL_DEV double iou_exact(const DevDet& a, const DevDet& b) {

@@ -243,6 +243,8 @@ void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, c
                     const double* bias, double thr, int cell_px, const Candidate* cand,
                     const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
                     int* det_count, long long cap_pf, int* overflow);
+void launch_score_dense(const Launch& L, const double* feat64, int cw, int ch, const double* w64, double bias,
+                        double* scores);
 void launch_score_exact_all(const Launch& L, const double* feat64, int cw, int ch, const double* w64,
                             double bias, double* scores);
 size_t nms_key_bytes();

@@ -14,6 +14,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <unistd.h>
@@ -336,6 +337,53 @@ static void gpu_tests(const std::string& model_path) {
   // detect + landmark in one device pass
   const auto both = gpu::detect_and_landmark({frame}, model, one);
   CHECK(both.size() == 1 && both[0].detections.size() == dets.size() && both[0].landmarks.size() == dets.size());
+  // ... and sharded over a device list (one B200 on the lease: the same device twice)
+  {
+    const auto multi = gpu::detect_and_landmark({frame, make_image(640, 480, 20.0), frame}, model, one, {0, 0});
+    bool eq = multi.size() == 3 && multi[1].detections.empty() && multi[0].detections.size() == dets.size() &&
+              multi[2].detections.size() == dets.size();
+    for (std::size_t k = 0; eq && k < dets.size(); ++k)
+      eq = multi[0].detections[k].score == dets[k].score && multi[2].detections[k].box.x == dets[k].box.x &&
+           multi[0].landmarks[k].points[1].y == both[0].landmarks[k].points[1].y;
+    CHECK(eq);
+  }
+  // a model edited in place (same object, same buffers): a split threshold change is seen by
+  // the next call (the content key hashes every split record)
+  {
+    ErtModel m = one;
+    const Shape before = predict_landmarks(half, Box{8, 8, 48, 48}, m);
+    m.cascade[0][0].splits[0].threshold = 1000.0;  // now Ia - Ib > thr fails: the other leaf
+    const Shape after = predict_landmarks(half, Box{8, 8, 48, 48}, m);
+    CHECK(before.points[0].x != after.points[0].x && std::fabs(after.points[0].x - (8 + 0.25 * 48 + 0.9 * 48)) < 1e-9);
+    m.cascade[0][0].leaves[1][0].x = -9.0;  // a leaf value edited in place: explicit invalidation
+    gpu::invalidate_model_cache();
+    const Shape again = predict_landmarks(half, Box{8, 8, 48, 48}, m);
+    CHECK(std::fabs(again.points[0].x - (8 + (0.25 - 0.9) * 48)) < 1e-9);
+  }
+  // score_dense in the definitional order vs score_separable (both bit-identical to the
+  // reference in their own order): a single non-zero weight makes them equal
+  {
+    FeatureImage fr2;
+    fr2.cells_w = 13;
+    fr2.cells_h = 12;
+    fr2.values.resize(13 * 12 * 31);
+    std::mt19937_64 r2(5);
+    for (double& v : fr2.values) v = urand(r2, 0.0, 0.4);
+    LinearFilter d1;
+    d1.weights[2 * 310 + 3 * 31 + 7] = 1.0;
+    const SaliencyMap a = score_dense(fr2, d1), b = score_separable(fr2, d1);
+    CHECK(a.scores == b.scores && a.scores[0] == fr2.cell(3, 2)[7]);
+  }
+  // concurrent callers on their own threads share the device models and agree bit for bit
+  {
+    std::vector<Shape> out(4);
+    std::vector<std::thread> th;
+    for (int t = 0; t < 4; ++t) th.emplace_back([&, t] { out[t] = predict_landmarks(half, Box{8, 8, 48, 48}, one); });
+    for (auto& t : th) t.join();
+    bool eq = true;
+    for (int t = 1; t < 4; ++t) eq = eq && out[t].points[0].x == out[0].points[0].x && out[t].points[1].y == out[0].points[1].y;
+    CHECK(eq && out[0].points[0].x == o.points[0].x);
+  }
 
   // run() over a frame directory: sequential == pipelined (test_pipeline.cpp:92-123)
   {

@@ -209,6 +209,15 @@ def test_score_golden(ctx):
     s = ctx.score_separable(g["feat"], g["weights"], float(g["bias"]))
     assert np.array_equal(s, g["separable"])
     assert np.max(np.abs(s - g["dense"])) <= 1e-4  # acceptance C1 contract
+    # score_dense in its own (definitional) order: bit-identical to the reference's
+    assert np.array_equal(ctx.score_dense(g["feat"], g["weights"], float(g["bias"])), g["dense"])
+
+
+def test_score_dense_random_vs_oracle(ctx, oracle):
+    feat = rng(71).uniform(0, 0.4, (23, 19, 31))
+    w = rng(72).uniform(-1, 1, 3100)
+    assert np.array_equal(ctx.score_dense(feat, w, 0.3), oracle.score_dense(feat, w, 0.3))
+    assert not np.array_equal(ctx.score_dense(feat, w, 0.3), ctx.score_separable(feat, w, 0.3))
 
 
 def test_score_known_answers(ctx):
