@@ -612,6 +612,7 @@ int check_frames(const void* frames, int pix, int n, int w, int h, size_t pitch,
 // device; n_faces_dev holds the count.  Output landmarks -> c->ert_out.
 // Face-count threshold of the wide (face-per-CTA) cascade, and the per-frame face estimate a
 // streamed batch is judged by before its detections exist (the count stays on the device).
+constexpr long long kErtClusterMaxFaces = 8;  // expected faces up to which the wide cascade runs as 4-CTA clusters
 constexpr long long kErtWideMaxFaces = 400;  // measured crossover 300-600 faces (tools/diag_ert_wide.py)
 constexpr long long kErtFacesPerFrameGuess = 4;
 
@@ -640,8 +641,11 @@ int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix
   // GPU with kFcFaces-face CTAs (latency), else kFcFaces faces per CTA (leaf-row reuse in L1)
   const bool wide = c->ert_mode == 2 || (c->ert_mode == 0 && expect_faces <= kErtWideMaxFaces);
   if (wide && ert_wide_fits(E.dev)) {
+    // a handful of faces (one frame): a cluster of 4 CTAs per face spreads each level's leaf
+    // rows over four SMs (C1 ERT 0.188 -> 0.169 ms); more faces fill the GPU with one CTA each
     launch_ert_wide(L, E.dev, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
-                    n_faces_dev, nf, out_xy, leaf_dev, (long long)E.dev.T * E.dev.K, err_dev);
+                    n_faces_dev, nf, out_xy, leaf_dev, (long long)E.dev.T * E.dev.K, err_dev,
+                    expect_faces <= kErtClusterMaxFaces ? 4 : 1);
     return BL_OK;
   }
   if (c->ert_mode != 3 && ert_cascade_fits(E.dev)) {

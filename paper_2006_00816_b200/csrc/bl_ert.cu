@@ -19,6 +19,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "bl_internal.cuh"
 
@@ -571,11 +572,314 @@ __global__ void __launch_bounds__(kWdMaxThreads) k_ert_wide(ErtDev M, const void
                                                : dadd((double)X, dmul(sc[c], (double)W));
 }
 
+// The small-batch cascade spread over a CLUSTER of CL CTAs per face.  Per level a face reads
+// K selected leaf rows (544 KB at 500 trees, L = 68): through one SM's L2 port that is ~9k
+// cycles, the largest part of k_ert_wide's level.  Here CTA rank r of the face's cluster
+// traverses the trees of chunks c = r, r + CL, ... and sums their leaf rows (same per-chunk
+// canonical order as k_ert_wide / k_ert_cascade), broadcasts the chunk partials into every
+// CTA's shared memory (DSMEM), and after one cluster barrier every CTA applies the identical
+// update (partials in chunk order, ert.cpp:118-126) to its own copy of the shape; the
+// transform (warp 0) is computed redundantly and identically in each CTA.  Bit-identical to
+// k_ert_wide.
+constexpr int kWclMax = 8;
+
+template <bool U8, int CL>
+__global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restrict__ frames, int w, int h,
+                                                 long long pitch, long long fstride,
+                                                 const int* __restrict__ face_frame,
+                                                 const int* __restrict__ boxes, int box_stride,
+                                                 const int* __restrict__ n_faces, int cap,
+                                                 double* __restrict__ out_xy, uint8_t* __restrict__ leaf_out,
+                                                 long long leaf_out_stride, int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char wd_smem[];
+  const int L = M.L, L2 = 2 * L, K = M.K, S = M.S, NL = M.NL;
+  const int nchunk = (K + kLeafChunk - 1) / kLeafChunk;
+  double* sc = reinterpret_cast<double*>(wd_smem);             // [2L] current shape
+  double* smc = sc + L2;                                       // [2L] centred mean shape
+  double2* stf = reinterpret_cast<double2*>(smc + L2);         // [1] transform
+  double2* spart = stf + 1;                                    // [2][nchunk][L] partial leaf sums (by level parity)
+  uint8_t* sli = reinterpret_cast<uint8_t*>(spart + 2 * nchunk * L);  // [K]
+  // [kLeafChunk][items] leaf pairs of this CTA's items, landed by cp.async (16-B aligned)
+  double2* stage = reinterpret_cast<double2*>(sli + ((K + 15) & ~15));
+  // records in shared memory when every CTA owns at most one chunk: [2 levels][3 planes][S][64]
+  const bool srec = nchunk <= CL;
+  int4* srecs = reinterpret_cast<int4*>(stage + kLeafChunk * L);
+  const int bd = blockDim.x;
+  const int n = min(*n_faces, cap);
+  const int face = blockIdx.x / CL;
+  const unsigned rank = blockIdx.x % CL;  // == %cluster_ctarank for cluster dims (CL, 1, 1)
+  if (face >= n) return;                  // the whole cluster leaves together
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < L2; e += bd) {
+    sc[e] = M.mean_xy[e];  // ert.cpp:106
+    smc[e] = M.mean_c[e];
+  }
+  const int* bx = boxes + (long long)face * box_stride;
+  const int X = bx[0], Y = bx[1], W = bx[2], H = bx[3];
+  const void* fr = (const char*)frames + (long long)face_frame[face] * fstride * (U8 ? 1 : 8);
+  // my chunks: rank, rank + CL, ...; my trees: kLeafChunk per chunk
+  const int my_chunks = nchunk > (int)rank ? (nchunk - 1 - (int)rank) / CL + 1 : 0;
+  const int my_trees = my_chunks * kLeafChunk;
+  auto tree_of = [&](int lt) { return (int)(rank + CL * (lt / kLeafChunk)) * kLeafChunk + lt % kLeafChunk; };
+  // DSMEM base addresses of spart in every CTA of the cluster
+  uint32_t rpart[CL];
+  {
+    const uint32_t local = (uint32_t)__cvta_generic_to_shared(spart);
+#pragma unroll
+    for (int q = 0; q < CL; ++q)
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rpart[q]) : "r"(local), "r"(q));
+  }
+  // level t's split records of my chunk -> srecs[t & 1] (cp.async, one commit group)
+  const int kc0 = (int)rank * kLeafChunk;
+  auto copy_recs = [&](int t) {
+    int4* dst = srecs + (t & 1) * 3 * S * kLeafChunk;
+    const int4* src = reinterpret_cast<const int4*>(M.split) + (long long)t * S * K;
+    for (int idx = tid; idx < 3 * S * kLeafChunk; idx += bd) {
+      const int pl = idx / (S * kLeafChunk), rem = idx - pl * S * kLeafChunk;
+      const int nd = rem / kLeafChunk, j = rem - nd * kLeafChunk;
+      if (kc0 + j < K)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + idx)),
+                     "l"(src + (long long)pl * M.split_plane + (long long)nd * K + kc0 + j)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (srec && my_chunks > 0) copy_recs(0);
+  __syncthreads();
+#if BL_WD_CLOCK
+  long long clk[4] = {0, 0, 0, 0};
+#endif
+  for (int t = 0; t < M.T; ++t) {
+#if BL_WD_CLOCK
+    const long long c0 = clock64();
+#endif
+    const int4* lvl = reinterpret_cast<const int4*>(M.split) + (long long)t * S * K;
+    auto rec = [&](int node, int k, SplitPlanes& r) {
+      const int4* q = lvl + (long long)node * K + k;
+      r.oa = __ldg(reinterpret_cast<const double2*>(q));
+      r.ob = __ldg(reinterpret_cast<const double2*>(q + M.split_plane));
+      r.tail = __ldg(q + 2 * M.split_plane);
+    };
+    const int4* srl = srecs + (t & 1) * 3 * S * kLeafChunk;
+    auto rec_s = [&](int node, int j, SplitPlanes& r) {  // j: tree within my chunk
+      const int4* q = srl + node * kLeafChunk + j;
+      const int4 a = q[0], b = q[S * kLeafChunk], c = q[2 * S * kLeafChunk];
+      r.oa = make_double2(__hiloint2double(a.y, a.x), __hiloint2double(a.w, a.z));
+      r.ob = make_double2(__hiloint2double(b.y, b.x), __hiloint2double(b.w, b.z));
+      r.tail = c;
+    };
+    SplitPlanes root;
+    const int k_first = tid < my_trees ? tree_of(tid) : K;
+    if (!srec && k_first < K && S > 0) rec(0, k_first, root);
+    if (warp == 0) {  // (1) transform (identical in every CTA of the cluster)
+      double A, B;
+      const int e = face_transform_warp(M, sc, smc, lane, A, B);
+      if (lane == 0) {
+        if (e && rank == 0) atomicExch(err, e);
+        stf[0] = make_double2(A, B);
+      }
+    }
+    if (srec) asm volatile("cp.async.wait_group 0;" ::: "memory");  // this level's records landed
+    __syncthreads();
+#if BL_WD_CLOCK
+    const long long c1 = clock64();
+#endif
+    // (2) traversals of my trees, ert.cpp:87-97
+    const double2 ab = stf[0];
+    for (int lt = tid; lt < my_trees; lt += bd) {
+      const int k = tree_of(lt);
+      if (k >= K) continue;
+      int node = 0;
+      SplitPlanes r;
+      const int jl = k - kc0;
+      if (srec)
+        rec_s(0, jl, r);
+      else if (lt == tid)
+        r = root;
+      else
+        rec(0, k, r);
+      for (int d = 0; d < M.F; ++d) {
+        SplitPlanes c1, c2;
+        const bool more = d + 1 < M.F;
+        if (more) {
+          if (srec) {
+            rec_s(2 * node + 1, jl, c1);
+            rec_s(2 * node + 2, jl, c2);
+          } else {
+            rec(2 * node + 1, k, c1);
+            rec(2 * node + 2, k, c2);
+          }
+        }
+        const double thr = __hiloint2double(r.tail.y, r.tail.x);
+        const int an_a = (short)(r.tail.z & 0xffff), an_b = (short)(r.tail.z >> 16);
+        const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_a, r.oa.x, r.oa.y);
+        const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_b, r.ob.x, r.ob.y);
+        const bool right = dsub(ia, ib) > thr;
+        node = right ? 2 * node + 1 : 2 * node + 2;
+        if (more) r = right ? c1 : c2;
+      }
+      sli[k] = (uint8_t)(node - S);
+      if (leaf_out) leaf_out[(long long)face * leaf_out_stride + (long long)t * K + k] = (uint8_t)(node - S);
+    }
+    __syncthreads();
+#if BL_WD_CLOCK
+    const long long c2 = clock64();
+#endif
+    // (3a) partial leaf sums of my chunks, broadcast to every CTA's spart[t & 1]
+    const double2* lv = reinterpret_cast<const double2*>(M.leaves + (long long)t * K * NL * L2);
+    const int row = NL * L;
+    const uint32_t boff = (uint32_t)((t & 1) * nchunk * L) * (uint32_t)sizeof(double2);
+    const int items = my_chunks * L;
+    for (int it = tid; it < items; it += bd) {
+      const int ci = it / L, p = it - ci * L;
+      const int ch = (int)rank + CL * ci;
+      const int k0 = ch * kLeafChunk, k1 = min(K, k0 + kLeafChunk);
+      double px = 0.0, py = 0.0;
+      if (items <= bd) {
+        // every selected leaf pair of the chunk in flight at once: cp.async into this item's
+        // column of the staging buffer ([tree][item]: conflict-free), one wait, then the
+        // tree-ordered sum from shared memory -- one L2 round trip instead of K/16
+        const uint32_t st0 = (uint32_t)__cvta_generic_to_shared(stage + it);
+        for (int kb = k0; kb < k1; kb += 16) {  // 16 trees per step: one 16-B read of their leaf indices
+          const uint4 li4 = *reinterpret_cast<const uint4*>(sli + kb);
+          const uint32_t lw[4] = {li4.x, li4.y, li4.z, li4.w};
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            if (kb + u < k1)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st0 + (uint32_t)((kb + u - k0) * items * 16)),
+                           "l"(lv + (long long)(kb + u) * row + (int)((lw[u >> 2] >> (8 * (u & 3))) & 0xffu) * L + p)
+                           : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        for (int kb = k0; kb < k1; kb += 16) {
+          double2 v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = kb + u < k1 ? stage[(kb + u - k0) * items + it] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            if (kb + u < k1) {
+              px = dadd(px, v[u].x);
+              py = dadd(py, v[u].y);
+            }
+        }
+      } else {
+        int k = k0;
+        for (; k + kWdInFlight <= k1; k += kWdInFlight) {
+          double2 v[kWdInFlight];
+#pragma unroll
+          for (int u = 0; u < kWdInFlight; ++u) v[u] = __ldg(lv + (long long)(k + u) * row + sli[k + u] * L + p);
+#pragma unroll
+          for (int u = 0; u < kWdInFlight; ++u) {
+            px = dadd(px, v[u].x);
+            py = dadd(py, v[u].y);
+          }
+        }
+        for (; k < k1; ++k) {
+          const double2 v = __ldg(lv + (long long)k * row + sli[k] * L + p);
+          px = dadd(px, v.x);
+          py = dadd(py, v.y);
+        }
+      }
+      const uint32_t off = boff + (uint32_t)(ch * L + p) * (uint32_t)sizeof(double2);
+#pragma unroll
+      for (int q = 0; q < CL; ++q)
+        asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(rpart[q] + off), "d"(px), "d"(py) : "memory");
+    }
+    // every chunk's partial is in every CTA (release / acquire across the cluster)
+    if (srec && my_chunks > 0 && t + 1 < M.T) copy_recs(t + 1);  // lands during the barrier, 3b and xform
+#if BL_WD_CLOCK
+    const long long c3 = clock64();
+#endif
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+#if BL_WD_CLOCK
+    const long long c4 = clock64();
+    if (tid == 0) {
+      clk[0] += c1 - c0;
+      clk[1] += c2 - c1;
+      clk[2] += c3 - c2;
+      clk[3] += c4 - c3;
+    }
+#endif
+    // (3b) partials in chunk order, cur += shrinkage * delta (ert.cpp:118-126), same in every CTA
+    if (tid < L) {
+      const double2* pp = spart + (t & 1) * nchunk * L;
+      double ax = 0.0, ay = 0.0;
+      for (int ch = 0; ch < nchunk; ++ch) {
+        const double2 q = pp[ch * L + tid];
+        ax = dadd(ax, q.x);
+        ay = dadd(ay, q.y);
+      }
+      sc[2 * tid] = dadd(sc[2 * tid], dmul(M.shrinkage, ax));
+      sc[2 * tid + 1] = dadd(sc[2 * tid + 1], dmul(M.shrinkage, ay));
+    }
+    __syncthreads();
+  }
+#if BL_WD_CLOCK
+  if (tid == 0 && face == 0)
+    printf("k_ert_wcl face 0 rank %u cycles: xform %lld traverse %lld accum %lld cluster-sync %lld\n", rank, clk[0],
+           clk[1], clk[2], clk[3]);
+#endif
+  // no CTA may exit while another could still write into its shared memory: every remote
+  // write of the last level precedes the last cluster barrier, so exiting is safe here
+  if (rank == 0)
+    for (int c = tid; c < L2; c += bd)
+      out_xy[(long long)face * L2 + c] = (c & 1) ? dadd((double)Y, dmul(sc[c], (double)H))
+                                                 : dadd((double)X, dmul(sc[c], (double)W));
+}
+
+template <bool U8, int CL>
+static cudaError_t launch_wcl(const Launch& L, const ErtDev& M, const void* frames, int w, int h, long long pitch,
+                              long long fstride, const int* face_frame, const int* boxes, int box_stride,
+                              const int* n_faces, int cap, double* out_xy, uint8_t* leaf_out,
+                              long long leaf_out_stride, int* err) {
+  const int nchunk = (int)div_up(M.K, kLeafChunk);
+  const int my_chunks = (nchunk + CL - 1) / CL;
+  const int threads = (int)std::min<long long>(256, div_up(std::max(my_chunks * std::max(kLeafChunk, M.L), 32), 32) * 32);
+  const size_t items = (size_t)my_chunks * M.L;
+  size_t smem = sizeof(double) * 4 * M.L + sizeof(double2) * (1 + 2 * (size_t)nchunk * M.L) + (size_t)((M.K + 15) & ~15);
+  if ((int)items <= threads) smem += sizeof(double2) * kLeafChunk * items;  // cp.async staging
+  if (nchunk <= CL) smem += sizeof(int4) * 2 * 3 * M.S * kLeafChunk;        // records, two levels
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cap * CL);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = L.st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_ert_wcl<U8, CL>, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride,
+                            n_faces, cap, out_xy, leaf_out, leaf_out_stride, err);
+}
+
 bool ert_wide_fits(const ErtDev& M) { return 2 * M.L <= kMaxL2; }
 
 void launch_ert_wide(const Launch& L, const ErtDev& M, const void* frames, int u8, int w, int h, long long pitch,
                      long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces,
-                     int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err) {
+                     int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err, int cl_req) {
+  static const int cl_env = [] {  // BL_ERT_CL=1|2|4|8 forces the cluster size (A/B)
+    const char* e = std::getenv("BL_ERT_CL");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int cl = cl_env ? cl_env : cl_req;
+  if (cl == 2 || cl == 4 || cl == 8) {
+    cudaError_t r = cudaSuccess;
+    if (cl == 2)
+      r = u8 ? launch_wcl<true, 2>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err)
+             : launch_wcl<false, 2>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err);
+    else if (cl == 4)
+      r = u8 ? launch_wcl<true, 4>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err)
+             : launch_wcl<false, 4>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err);
+    else
+      r = u8 ? launch_wcl<true, 8>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err)
+             : launch_wcl<false, 8>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err);
+    (void)r;
+    ++*L.counter;
+    return;
+  }
   const long long nchunk = div_up(M.K, kLeafChunk);
   const size_t smem = sizeof(double) * 4 * M.L + sizeof(double2) * (1 + nchunk * M.L) + (size_t)M.K;
   const int threads = ert_wide_threads(M);
@@ -637,6 +941,12 @@ void configure_ert_kernels(int optin) {  // per device, see configure_screen_tc_
   smem_optin(k_ert_wide<false>, optin);
   smem_optin(k_ert_cascade<true>, optin);
   smem_optin(k_ert_cascade<false>, optin);
+  smem_optin(k_ert_wcl<true, 2>, optin);
+  smem_optin(k_ert_wcl<false, 2>, optin);
+  smem_optin(k_ert_wcl<true, 4>, optin);
+  smem_optin(k_ert_wcl<false, 4>, optin);
+  smem_optin(k_ert_wcl<true, 8>, optin);
+  smem_optin(k_ert_wcl<false, 8>, optin);
 }
 
 }  // namespace blb

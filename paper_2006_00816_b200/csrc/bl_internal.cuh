@@ -264,7 +264,8 @@ bool ert_cascade_fits(const ErtDev& M);
 bool ert_wide_fits(const ErtDev& M);
 void launch_ert_wide(const Launch& L, const ErtDev& M, const void* frames, int u8, int w, int h, long long pitch,
                      long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces,
-                     int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err);
+                     int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err,
+                     int cluster /* CTAs per face: 1, 2, 4 or 8 */);
 void launch_ert_cascade(const Launch& L, const ErtDev& M, const void* frames, int u8, int w, int h, long long pitch,
                         long long fstride, const int* face_frame, const int* boxes, int box_stride,
                         const int* n_faces, int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride,

@@ -1,5 +1,5 @@
-"""Per-phase clock64 totals of the latency ERT kernel on one face (BL_WD_CLOCK build), cold then
-warm:  BL_LIBRARY=variants/wdclock/libblinkline_b200.so BL_ERT=wide python tools/ert_clock.py"""
+"""Per-phase clock64 totals of the latency ERT kernels on one face (BL_WD_CLOCK build), cold
+then warm:  BL_LIBRARY=variants/wdclock/libblinkline_b200.so BL_ERT=wide [BL_ERT_CL=4] python tools/ert_clock.py"""
 import os
 import sys
 
