@@ -56,6 +56,7 @@ BL_DEV double sample_px(const void* fr, int w, int h, long long pitch, int bx, i
   return __ldg((const double*)fr + (long long)iy * pitch + ix);
 }
 
+template <bool SINCOS = false>
 __device__ int face_transform_warp(const ErtDev& M, const double* c, const double* mc, int lane, double& A,
                                    double& B);
 
@@ -106,6 +107,7 @@ BL_DEV double warp_sum(double v) {
 // (c, mc: the current shape and the centred mean shape, shared or global).  Returns 0 or the
 // reference's error (1: source shape has no spread, 2: target shape has no spread) and the
 // linear part (scale*cos, scale*sin) in A, B; identical in every lane.
+template <bool SINCOS>
 __device__ int face_transform_warp(const ErtDev& M, const double* c, const double* mc, int lane, double& A,
                                    double& B) {
   const int L = M.L;
@@ -133,15 +135,26 @@ __device__ int face_transform_warp(const ErtDev& M, const double* c, const doubl
   const double a = ddiv(sre, sff), b = ddiv(sim, sff);
   // ert.cpp:60-67, the three libm chains on different lanes (same functions, same results):
   // lane 2 scale = hypot(a, b); lanes 0 / 1 rot = atan2(b, a) then cos / sin
-  double v;
-  if (lane == 2) {
-    v = hypot(a, b);
-  } else {
-    const double rot = atan2(b, a);
-    v = lane == 1 ? sin(rot) : cos(rot);
+  double v, sr, cr;
+  if (SINCOS) {  // latency kernels: one shared argument reduction, no divergent sin / cos lanes
+    if (lane == 2) {
+      v = hypot(a, b);
+    } else {
+      sincos(atan2(b, a), &sr, &cr);
+    }
+    cr = __shfl_sync(0xffffffffu, cr, 0);
+    sr = __shfl_sync(0xffffffffu, sr, 0);
+  } else {  // (fewer registers: the 4-face cascade's occupancy)
+    if (lane == 2) {
+      v = hypot(a, b);
+    } else {
+      const double rot = atan2(b, a);
+      v = lane == 1 ? sin(rot) : cos(rot);
+    }
+    cr = __shfl_sync(0xffffffffu, v, 0);
+    sr = __shfl_sync(0xffffffffu, v, 1);
   }
   const double scale = __shfl_sync(0xffffffffu, v, 2);
-  const double cr = __shfl_sync(0xffffffffu, v, 0), sr = __shfl_sync(0xffffffffu, v, 1);
   if (!(scale > 0.0)) return 2;  // "target shape has no spread" (ert.cpp:62-63)
   A = dmul(scale, cr);
   B = dmul(scale, sr);
@@ -413,6 +426,9 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
 //            the partials in chunk order, cur += shrinkage * delta.
 // The leaf sum of a level is then ~kLeafChunk dependent adds and loads deep instead of K.
 // Same canonical order as k_ert_cascade / k_ert_accum (bit-identical to both).
+#ifndef BL_ERT_WIDE_SINCOS
+#define BL_ERT_WIDE_SINCOS 0
+#endif
 #ifndef BL_WD_CLOCK
 #define BL_WD_CLOCK 0  // per-phase clock64 totals of face 0, printed (experiments)
 #endif
@@ -476,7 +492,7 @@ __global__ void __launch_bounds__(kWdMaxThreads) k_ert_wide(ErtDev M, const void
 #endif
     if (warp == 0) {  // (1) transform
       double A, B;
-      const int e = face_transform_warp(M, sc, smc, lane, A, B);
+      const int e = face_transform_warp<BL_ERT_WIDE_SINCOS>(M, sc, smc, lane, A, B);
       if (lane == 0) {
         if (e) atomicExch(err, e);
         stf[0] = make_double2(A, B);
@@ -582,6 +598,9 @@ __global__ void __launch_bounds__(kWdMaxThreads) k_ert_wide(ErtDev M, const void
 // transform (warp 0) is computed redundantly and identically in each CTA.  Bit-identical to
 // k_ert_wide.
 constexpr int kWclMax = 8;
+#ifndef BL_ERT_SREC
+#define BL_ERT_SREC 0  // split records of the level staged in shared memory (cluster kernel)
+#endif
 
 template <bool U8, int CL>
 __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restrict__ frames, int w, int h,
@@ -601,9 +620,9 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
   uint8_t* sli = reinterpret_cast<uint8_t*>(spart + 2 * nchunk * L);  // [K]
   // [kLeafChunk][items] leaf pairs of this CTA's items, landed by cp.async (16-B aligned)
   double2* stage = reinterpret_cast<double2*>(sli + ((K + 15) & ~15));
-  // records in shared memory when every CTA owns at most one chunk: [2 levels][3 planes][S][64]
-  const bool srec = nchunk <= CL;
-  int4* srecs = reinterpret_cast<int4*>(stage + kLeafChunk * L);
+  // the level's split records of my trees, [3 planes][S][my trees], share the staging
+  // buffer (records live during the traversal, leaf pairs during the accumulation)
+  int4* srecs = reinterpret_cast<int4*>(stage);
   const int bd = blockDim.x;
   const int n = min(*n_faces, cap);
   const int face = blockIdx.x / CL;
@@ -620,6 +639,7 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
   // my chunks: rank, rank + CL, ...; my trees: kLeafChunk per chunk
   const int my_chunks = nchunk > (int)rank ? (nchunk - 1 - (int)rank) / CL + 1 : 0;
   const int my_trees = my_chunks * kLeafChunk;
+  const bool srec = BL_ERT_SREC && my_chunks * L <= bd && 3 * S * my_trees * 16 <= kLeafChunk * my_chunks * L * 16;
   auto tree_of = [&](int lt) { return (int)(rank + CL * (lt / kLeafChunk)) * kLeafChunk + lt % kLeafChunk; };
   // DSMEM base addresses of spart in every CTA of the cluster
   uint32_t rpart[CL];
@@ -629,17 +649,17 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
     for (int q = 0; q < CL; ++q)
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rpart[q]) : "r"(local), "r"(q));
   }
-  // level t's split records of my chunk -> srecs[t & 1] (cp.async, one commit group)
-  const int kc0 = (int)rank * kLeafChunk;
+  // level t's split records of my trees -> srecs (cp.async, one commit group)
   auto copy_recs = [&](int t) {
-    int4* dst = srecs + (t & 1) * 3 * S * kLeafChunk;
     const int4* src = reinterpret_cast<const int4*>(M.split) + (long long)t * S * K;
-    for (int idx = tid; idx < 3 * S * kLeafChunk; idx += bd) {
-      const int pl = idx / (S * kLeafChunk), rem = idx - pl * S * kLeafChunk;
-      const int nd = rem / kLeafChunk, j = rem - nd * kLeafChunk;
-      if (kc0 + j < K)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + idx)),
-                     "l"(src + (long long)pl * M.split_plane + (long long)nd * K + kc0 + j)
+    const int per_plane = S * my_trees;
+    for (int idx = tid; idx < 3 * per_plane; idx += bd) {
+      const int pl = idx / per_plane, rem = idx - pl * per_plane;
+      const int nd = rem / my_trees, lt = rem - nd * my_trees;
+      const int k = tree_of(lt);
+      if (k < K)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(srecs + idx)),
+                     "l"(src + (long long)pl * M.split_plane + (long long)nd * K + k)
                      : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -660,10 +680,9 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
       r.ob = __ldg(reinterpret_cast<const double2*>(q + M.split_plane));
       r.tail = __ldg(q + 2 * M.split_plane);
     };
-    const int4* srl = srecs + (t & 1) * 3 * S * kLeafChunk;
-    auto rec_s = [&](int node, int j, SplitPlanes& r) {  // j: tree within my chunk
-      const int4* q = srl + node * kLeafChunk + j;
-      const int4 a = q[0], b = q[S * kLeafChunk], c = q[2 * S * kLeafChunk];
+    auto rec_s = [&](int node, int lt, SplitPlanes& r) {  // lt: my local tree index
+      const int4* q = srecs + node * my_trees + lt;
+      const int4 a = q[0], b = q[S * my_trees], c = q[2 * S * my_trees];
       r.oa = make_double2(__hiloint2double(a.y, a.x), __hiloint2double(a.w, a.z));
       r.ob = make_double2(__hiloint2double(b.y, b.x), __hiloint2double(b.w, b.z));
       r.tail = c;
@@ -673,7 +692,7 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
     if (!srec && k_first < K && S > 0) rec(0, k_first, root);
     if (warp == 0) {  // (1) transform (identical in every CTA of the cluster)
       double A, B;
-      const int e = face_transform_warp(M, sc, smc, lane, A, B);
+      const int e = face_transform_warp<BL_ERT_WIDE_SINCOS>(M, sc, smc, lane, A, B);
       if (lane == 0) {
         if (e && rank == 0) atomicExch(err, e);
         stf[0] = make_double2(A, B);
@@ -691,7 +710,7 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
       if (k >= K) continue;
       int node = 0;
       SplitPlanes r;
-      const int jl = k - kc0;
+      const int jl = lt;
       if (srec)
         rec_s(0, jl, r);
       else if (lt == tid)
@@ -786,7 +805,10 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
         asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(rpart[q] + off), "d"(px), "d"(py) : "memory");
     }
     // every chunk's partial is in every CTA (release / acquire across the cluster)
-    if (srec && my_chunks > 0 && t + 1 < M.T) copy_recs(t + 1);  // lands during the barrier, 3b and xform
+    if (srec && t + 1 < M.T) {  // next level's records into the (now free) staging buffer:
+      __syncthreads();          // they land during the cluster barrier, the update and the transform
+      copy_recs(t + 1);
+    }
 #if BL_WD_CLOCK
     const long long c3 = clock64();
 #endif
@@ -838,7 +860,7 @@ static cudaError_t launch_wcl(const Launch& L, const ErtDev& M, const void* fram
   const size_t items = (size_t)my_chunks * M.L;
   size_t smem = sizeof(double) * 4 * M.L + sizeof(double2) * (1 + 2 * (size_t)nchunk * M.L) + (size_t)((M.K + 15) & ~15);
   if ((int)items <= threads) smem += sizeof(double2) * kLeafChunk * items;  // cp.async staging
-  if (nchunk <= CL) smem += sizeof(int4) * 2 * 3 * M.S * kLeafChunk;        // records, two levels
+  // (the split records of a level share the staging buffer when they fit, see k_ert_wcl)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cap * CL);
   cfg.blockDim = dim3(threads);
