@@ -559,7 +559,7 @@ int record_detect(bl_ctx* c, const void* in, int pix, int n, long long pitch, lo
     launch_screen(L, P.host, Pd, P.feat32.as<float>(), D.w32.as<float>(), D.cut32.as<float>(),
                   P.cand.as<Candidate>(), P.n_cand.as<unsigned long long>(), P.cand_cap);
   stage_mark(c, BL_STAGE_RESCORE);
-  launch_rescore(L, Pd, P.feat64.as<double>(), D.w64.as<double>(), D.bias64.as<double>(), D.thr, D.cell_px,
+  launch_rescore(L, n, Pd, P.feat64.as<double>(), D.w64.as<double>(), D.bias64.as<double>(), D.thr, D.cell_px,
                  P.cand.as<Candidate>(), P.n_cand.as<unsigned long long>(), P.cand_cap, P.dets.as<DevDet>(),
                  P.det_count.as<int>(), P.cap_pf, P.overflow.as<int>());
   stage_mark(c, BL_STAGE_NMS);

@@ -70,9 +70,28 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __res
   const long long n = min((long long)*n_cand, cand_cap);
   if (n == 0) return;
   double* Wsm = rs_smem + (size_t)kRsWarps * kRsWarpDoubles;  // [5][10][311]
-  for (int e = threadIdx.x; e < kFilters * kFilterW; e += blockDim.x) {
-    const int rj = e / kRowW;  // r * 10 + j
-    Wsm[rj * kRsWPitch + (e - rj * kRowW)] = __ldg(w64 + e);
+  {  // stage the weights: 128-bit loads, 8 in flight per thread (a row of 310 is even, so a
+     // pair never straddles two rows); one load at a time made this most of a small batch's time
+    constexpr int kPairs = kFilters * kFilterW / 2, kU = 8;
+    const double2* w2 = reinterpret_cast<const double2*>(w64);
+    for (int e0 = threadIdx.x; e0 < kPairs; e0 += blockDim.x * kU) {
+      double2 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * blockDim.x;
+        v[u] = e < kPairs ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = 2 * (e0 + u * blockDim.x);
+        if (e < kFilters * kFilterW) {
+          const int rj = e / kRowW;  // r * 10 + j
+          double* d = Wsm + rj * kRsWPitch + (e - rj * kRowW);
+          d[0] = v[u].x;
+          d[1] = v[u].y;
+        }
+      }
+    }
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -113,15 +132,13 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __res
         double fr[kFeat];
 #pragma unroll
         for (int f = 0; f < kFeat; ++f) fr[f] = Fs[lane * kRsPitch + f];
+        // all five filters' chains, branch-free and interleaved (five independent dependent-add
+        // chains in flight instead of one); a filter outside the mask is computed and discarded
 #pragma unroll
-        for (int r = 0; r < kFilters; ++r) {
-          if (!((mask_any >> r) & 1u)) continue;  // warp-uniform
-          const double* wr = wrow + r * kWin * kRsWPitch + ci * kFeat;
-          double a = acc[r];
+        for (int f = 0; f < kFeat; ++f)
 #pragma unroll
-          for (int f = 0; f < kFeat; ++f) a = dadd(a, dmul(fr[f], wr[f]));  // detector.cpp:84
-          acc[r] = a;
-        }
+          for (int r = 0; r < kFilters; ++r)
+            acc[r] = dadd(acc[r], dmul(fr[f], wrow[r * kWin * kRsWPitch + ci * kFeat + f]));  // detector.cpp:84
       }
       __syncwarp();
     }
@@ -157,14 +174,18 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __res
   }
 }
 
-void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, const double* w64,
+constexpr int kRsCtasPerFrame = 8;
+void launch_rescore(const Launch& L, int n_frames, const PlanDesc* Pd, const double* feat64, const double* w64,
                     const double* bias, double thr, int cell_px, const Candidate* cand,
                     const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
                     int* det_count, long long cap_pf, int* overflow) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const dim3 grid((unsigned)sms);  // persistent: one CTA per SM (the weights fill most of its smem)
+  // persistent: one CTA per SM (the weights fill most of its smem), but a small batch takes
+  // fewer: every CTA stages all 124 KB of weights, and for a frame or two that staging, not the
+  // few hundred candidates, is the kernel's time (C1: 27 us at 148 CTAs)
+  const dim3 grid((unsigned)std::max(1, std::min(sms, n_frames * kRsCtasPerFrame)));
   k_rescore<<<grid, 32 * kRsWarps, kRsSmem, L.st>>>(Pd, feat64, w64, bias, thr, cell_px, cand, n_cand, cand_cap,
                                                     dets, det_count, cap_pf, overflow);
   ++*L.counter;
@@ -427,7 +448,10 @@ __global__ void __launch_bounds__(256) k_nms(const DevDet* __restrict__ dets,
 // the round's newly kept boxes in parallel.  Rounds ~ kept / batch, not n, so a frame with
 // a thousand raw detections and a handful of faces takes a few microseconds.
 constexpr int kNmsSmallMax = 2048;
-constexpr int kNmsSmallThreads = 1024;
+#ifndef BL_NMS_SMALL_THREADS
+#define BL_NMS_SMALL_THREADS 256  // (1024: barriers over 32 warps dominated a 200-box frame)
+#endif
+constexpr int kNmsSmallThreads = BL_NMS_SMALL_THREADS;
 
 size_t nms_small_smem_bytes() {
   return sizeof(NmsKey) * kNmsSmallMax + sizeof(uint32_t) * (kNmsSmallMax / 32 + 32 + 32 + 8);
@@ -527,12 +551,12 @@ __global__ void __launch_bounds__(kNmsSmallThreads) k_nms_small(const DevDet* __
     __syncthreads();
     const int nc = ctl[0];
     if (nc == 0) break;
-    {  // overlap matrix of the candidates: warp a, lane b < a
-      const int a = warp, b = lane;
+    for (int a = warp; a < 32; a += kNmsSmallThreads / 32) {  // overlap matrix of the candidates: row a, lane b < a
+      const int b = lane;
       bool o = false;
       if (a < nc && b < a) o = iou_exceeds(sorted[cand[b]], sorted[cand[a]], iou_thr);
       const uint32_t m = __ballot_sync(0xffffffffu, o);
-      if (lane == 0 && a < 32) ovl[a] = m;
+      if (lane == 0) ovl[a] = m;
     }
     __syncthreads();
     if (tid == 0) {  // resolve the batch in order; candidates become processed

@@ -239,7 +239,7 @@ void launch_screen_tc(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, c
                       const float* w_tc, const float* cut, Candidate* cand, unsigned long long* n_cand,
                       long long cand_cap, float* dbg_scores);
 // bl_exact.cu
-void launch_rescore(const Launch& L, const PlanDesc* Pd, const double* feat64, const double* w64,
+void launch_rescore(const Launch& L, int n_frames, const PlanDesc* Pd, const double* feat64, const double* w64,
                     const double* bias, double thr, int cell_px, const Candidate* cand,
                     const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
                     int* det_count, long long cap_pf, int* overflow);
