@@ -180,6 +180,10 @@ struct Plan {
   long long gkeys_pf = 0;
   DevBuf arena, bins, energy, feat64, feat32, feat_tc, cand, n_cand, dets, det_count, kept, kept_count, gkeys,
       overflow, offsets;
+  // level 0's gradHist reads only the caller's frames: it runs on `aux` beside the pyramid
+  // (fork / join events, capturable into the batch's graph)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // ERT cascade working set (current shapes, per-level transforms, leaf-index scratch).
@@ -486,6 +490,16 @@ int record_detect(bl_ctx* c, const void* in, int pix, int n, long long pitch, lo
   Plan& P = *c->plan;
   const Launch L = launch_of(c);
   const DetectorState& D = (*c->detp);
+  // level 0 scored (small frames, e.g. the 320x240 camera stream): its gradHist needs only the
+  // caller's frames, so it runs on the plan's side stream beside the pyramid
+  const bool fork0 = !c->timing && !P.scored.empty() && P.scored[0] == 0 && P.aux;
+  if (fork0) {
+    CK(cudaEventRecord(P.ev_fork, c->st));
+    CK(cudaStreamWaitEvent(P.aux, P.ev_fork, 0));
+    launch_hog(Launch{P.aux, &c->launches}, P.host, P.desc.as<PlanDesc>(), 0, 1, in, pix == BL_PIX_U8 ? 0 : 1,
+               P.bins.as<double>(), P.energy.as<double>());
+    CK(cudaEventRecord(P.ev_join, P.aux));
+  }
   stage_mark(c, BL_STAGE_PYRAMID);
   // pyramid chain (image.cpp:162-170): level k from level k-1, every frame at once.  A level
   // no window scores (below the smallest eligible face) is read only by the next step, so
@@ -542,10 +556,12 @@ int record_detect(bl_ctx* c, const void* in, int pix, int n, long long pitch, lo
     // fused gradient + histogram + energy (the gradient field stays on chip)
     int s1 = 0;
     if (P.scored[0] == 0) {  // level 0 reads the caller's frames (u8 or f64)
-      launch_hog(L, P.host, Pd, 0, 1, in, pix == BL_PIX_U8 ? 0 : 1, P.bins.as<double>(), P.energy.as<double>());
+      if (!fork0)
+        launch_hog(L, P.host, Pd, 0, 1, in, pix == BL_PIX_U8 ? 0 : 1, P.bins.as<double>(), P.energy.as<double>());
       s1 = 1;
     }
     launch_hog(L, P.host, Pd, s1, ns, P.arena.as<double>(), 1, P.bins.as<double>(), P.energy.as<double>());
+    if (fork0) CK(cudaStreamWaitEvent(c->st, P.ev_join, 0));
   }
   stage_mark(c, BL_STAGE_FEATURES);
   const bool tc = P.screen == BL_SCREEN_TCGEN05;
@@ -1141,6 +1157,11 @@ int bl_ctx_create(int device, bl_ctx** out) {
   c->st = c->user = c->own;
   for (int l = 1; l < kLanes; ++l) CK(cudaStreamCreateWithFlags(&c->lanes[l], cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_lane, cudaEventDisableTiming));
+  for (Plan& P : c->plans) {
+    CK(cudaStreamCreateWithFlags(&P.aux, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&P.ev_join, cudaEventDisableTiming));
+  }
   for (Slot& S : c->slots) {
     CK(cudaStreamCreateWithFlags(&S.d2h, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&S.ev_h2d, cudaEventDisableTiming));
@@ -1189,6 +1210,14 @@ void bl_ctx_destroy(bl_ctx* c) {
   for (int l = 1; l < kLanes; ++l)
     if (c->lanes[l]) cudaStreamSynchronize(c->lanes[l]);
   if (c->ev_lane) cudaEventDestroy(c->ev_lane);
+  for (Plan& P : c->plans) {
+    if (P.aux) {
+      cudaStreamSynchronize(P.aux);
+      cudaStreamDestroy(P.aux);
+    }
+    for (cudaEvent_t e : {P.ev_fork, P.ev_join})
+      if (e) cudaEventDestroy(e);
+  }
   for (Slot& S : c->slots) {
     if (S.h_meta) cudaFreeHost(S.h_meta);
     if (S.h_stage) cudaFreeHost(S.h_stage);
