@@ -9,7 +9,8 @@ invariance), and repeated runs are bit-identical (determinism).
   C2  320x240 eyeblink stream, batch 16
   C3  1280x720, batch 64, full pyramid
   C4  landmark-only: 10k face boxes, 15-cascade x 500-tree depth-4 random-init ERT
-  C5  1920x1080, batch 256 per GPU (here 32 + 8 checked)"""
+  C5  1920x1080, batch 256 per GPU: the full batch, three frames checked against the
+      oracle, batch invariance against one-frame batches (and a 32-frame determinism case)"""
 
 import numpy as np
 import pytest
@@ -96,6 +97,33 @@ def test_c5_1080p_batch(ctx, oracle, pattern_model):
     again = ctx.detect_landmarks(frames)
     for k in range(32):
         assert np.array_equal(again[0][k], dets[k]) and np.array_equal(again[1][k], lms[k])
+
+
+def test_c5_1080p_full_batch256(ctx, oracle, pattern_model):
+    """C5 at its stated batch: 256 1920x1080 frames in one call (16 distinct ring frames
+    cycled, so generation stays fast), with the bench's 15 x 500 x depth-4 cascade; frames 5,
+    130 and 255 against the oracle, and the same frames as one-frame batches."""
+    base = ring_frames_np(16, 1920, 1080, seed=515)
+    frames = np.ascontiguousarray(base[np.arange(256) % 16])
+    ert = random_ert(T=15, K=500, F=4, seed=2020)
+    ctx.upload_detector(pattern_model)
+    ctx.upload_ert(ert)
+    dets, lms, faces = _check_frames(ctx, oracle, pattern_model, ert, frames, [5, 130, 255])
+    assert faces > 0 and sum(len(d) for d in dets) >= 256
+    for k in (5, 130, 255):
+        d1, l1 = ctx.detect_landmarks(frames[k:k + 1])
+        assert np.array_equal(d1[0], dets[k]) and np.array_equal(l1[0], lms[k])
+
+
+def test_bench_workload_vs_oracle(ctx, oracle, pattern_model):
+    """bench.py's exact workload: 512 640x480 ring frames in one call with the 15 x 500 x
+    depth-4 cascade (seed 2020) on every kept detection; three frames against the oracle."""
+    frames = ring_frames_np(512, 640, 480, seed=1000)
+    ert = random_ert(T=15, K=500, F=4, seed=2020)
+    ctx.upload_detector(pattern_model)
+    ctx.upload_ert(ert)
+    dets, lms, faces = _check_frames(ctx, oracle, pattern_model, ert, frames, [0, 257, 511])
+    assert faces > 0 and sum(len(d) for d in dets) > 512
 
 
 def test_bench_batch_vs_small_batch_kernels(ctx, pattern_model):
