@@ -252,6 +252,8 @@ struct bl_ctx {
   float stage_ms[BL_STAGE_COUNT] = {};
   int stage_launch[BL_STAGE_COUNT] = {};
   bool graphs = true;
+  bool ert_serial = false;          // BL_ERT_SERIAL=1: the cascade on the lane stream (experiment)
+  int lanes_large = kLanesLarge;    // BL_LANES_LARGE: detection lanes for large batches (experiment)
   cudaStream_t hst = nullptr;  // H2D stream (input frames): never queued behind a D2H wait
   // CUDA graphs (bl_ctx_enable_graphs): a batch's detection launches (one graph per lane plan,
   // slot and input) and its landmark cascade (one per slot and input) are captured once on a
@@ -876,9 +878,14 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
   }
   if (landmarks) {
     stage_mark(c, BL_STAGE_ERT);
-    // the cascade only reads this slot's buffers and the frames, so (unless per-stage timing
-    // wants one ordered stream) it runs on the ERT stream while the next batch detects
-    cudaStream_t es = c->timing ? c->st : S.est;
+    // the cascade only reads this slot's buffers and the frames.  A small batch's cascade runs
+    // on the slot's ERT stream, beside the next batches' detection and the other slots'
+    // cascades (few faces fill few SMs: C2 14k -> 64k frames/s with this).  A large batch's
+    // cascade runs after its own detection on the lane stream: beside the other lane's
+    // detection its 130 MB leaf table and the detection's streams evict each other from L2 --
+    // measured 86-89k frames/s at the bench concurrent, 99-102k queued on the lane.
+    const bool large = (long long)n * w * h > kSmallBatchPx;
+    cudaStream_t es = (c->timing || c->ert_serial || large) ? c->st : S.est;
     if (es != c->st) {
       CK(cudaEventRecord(S.ev_det, c->st));
       CK(cudaStreamWaitEvent(es, S.ev_det, 0));
@@ -1192,6 +1199,8 @@ int bl_ctx_create(int device, bl_ctx** out) {
   if (const char* e = std::getenv("BL_SCREEN")) c->screen = std::strcmp(e, "fp32") == 0 ? BL_SCREEN_FP32 : BL_SCREEN_TCGEN05;
   if (const char* e = std::getenv("BL_PYR_FUSE")) c->pyr_fuse = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_GRAPHS")) c->graphs = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BL_ERT_SERIAL")) c->ert_serial = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BL_LANES_LARGE")) c->lanes_large = std::max(1, std::min(kLanes, std::atoi(e)));
   if (const char* e = std::getenv("BL_PYR_CHAIN")) c->pyr_chain = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT"))
     c->ert_mode = !std::strcmp(e, "cascade") ? 1 : !std::strcmp(e, "wide") ? 2 : !std::strcmp(e, "levels") ? 3 : 0;
@@ -1558,7 +1567,7 @@ int bl_submit(bl_ctx* c, const void* frames, int pixel_type, int n, int w, int h
   const int s = (int)(t % BL_MAX_IN_FLIGHT);
   if (c->slots[s].busy)
     return set_err(BL_ERR_STATE, "%d batches in flight: collect one before submitting", BL_MAX_IN_FLIGHT);
-  const int n_lanes = (long long)n * w * h <= kSmallBatchPx ? kLanes : kLanesLarge;
+  const int n_lanes = (long long)n * w * h <= kSmallBatchPx ? kLanes : c->lanes_large;
   const int lane = c->timing ? 0 : (int)(t % n_lanes);
   if (lane > 0) {  // after whatever the caller queued on its stream (e.g. device-resident inputs)
     CK(cudaEventRecord(c->ev_lane, c->user));
