@@ -253,6 +253,7 @@ struct bl_ctx {
   int stage_launch[BL_STAGE_COUNT] = {};
   bool graphs = true;
   bool ert_serial = false;          // BL_ERT_SERIAL=1: the cascade on the lane stream (experiment)
+  bool ert_conc = false;            // BL_ERT_CONC=1: large batches' cascades concurrent again (experiment)
   int lanes_large = kLanesLarge;    // BL_LANES_LARGE: detection lanes for large batches (experiment)
   cudaStream_t hst = nullptr;  // H2D stream (input frames): never queued behind a D2H wait
   // CUDA graphs (bl_ctx_enable_graphs): a batch's detection launches (one graph per lane plan,
@@ -885,7 +886,7 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
     // detection its 130 MB leaf table and the detection's streams evict each other from L2 --
     // measured 86-89k frames/s at the bench concurrent, 99-102k queued on the lane.
     const bool large = (long long)n * w * h > kSmallBatchPx;
-    cudaStream_t es = (c->timing || c->ert_serial || large) ? c->st : S.est;
+    cudaStream_t es = (c->timing || c->ert_serial || (large && !c->ert_conc)) ? c->st : S.est;
     if (es != c->st) {
       CK(cudaEventRecord(S.ev_det, c->st));
       CK(cudaStreamWaitEvent(es, S.ev_det, 0));
@@ -1200,6 +1201,7 @@ int bl_ctx_create(int device, bl_ctx** out) {
   if (const char* e = std::getenv("BL_PYR_FUSE")) c->pyr_fuse = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_GRAPHS")) c->graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT_SERIAL")) c->ert_serial = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BL_ERT_CONC")) c->ert_conc = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_LANES_LARGE")) c->lanes_large = std::max(1, std::min(kLanes, std::atoi(e)));
   if (const char* e = std::getenv("BL_PYR_CHAIN")) c->pyr_chain = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT"))

@@ -39,6 +39,16 @@ void launch_ert_init(const Launch& L, const ErtDev& M, const int* n_faces, int c
   ++*L.counter;
 }
 
+#ifndef BL_ERT_EVICT_LAST
+#define BL_ERT_EVICT_LAST 0  // leaf rows loaded with an L2 evict_last policy (experiment)
+#endif
+BL_DEV double2 ld_leaf(const double2* p, uint64_t pol) {
+  if (!BL_ERT_EVICT_LAST) return __ldg(p);
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
 template <bool U8>
 BL_DEV double sample_px(const void* fr, int w, int h, long long pitch, int bx, int by, int bw, int bh,
                         const double* cur, double A, double B, int anchor, double ox, double oy) {
@@ -373,6 +383,8 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
     }
     __syncthreads();
     // (3) leaf sums in tree order, cur += shrinkage * delta (ert.cpp:118-126)
+    uint64_t pol = 0;
+    if (BL_ERT_EVICT_LAST) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     if (tid < nf * L) {
       const int fi = tid / L, p = tid - fi * L;
       const uint8_t* li = sli + fi * K;
@@ -386,7 +398,7 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
         for (; k + 16 <= c1; k += 16) {
           double2 v[16];
 #pragma unroll
-          for (int u = 0; u < 16; ++u) v[u] = __ldg(lv + (k + u) * row + li[k + u] * L);
+          for (int u = 0; u < 16; ++u) v[u] = ld_leaf(lv + (k + u) * row + li[k + u] * L, pol);
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             px = dadd(px, v[u].x);
@@ -394,7 +406,7 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
           }
         }
         for (; k < c1; ++k) {
-          const double2 v = __ldg(lv + k * row + li[k] * L);
+          const double2 v = ld_leaf(lv + k * row + li[k] * L, pol);
           px = dadd(px, v.x);
           py = dadd(py, v.y);
         }
