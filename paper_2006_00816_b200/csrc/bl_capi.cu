@@ -150,7 +150,7 @@ struct DetectorState {
   float cut[kFilters] = {0};
   float cut_tc[2 * kFilters] = {0};  // [0, 5): cut in the screen's scaled domain, [5, 10): 2^-scale
   double delta_tc[kFilters] = {0};
-  DevBuf w64, w32, bias64, cut32, w_tc, cuttc;
+  DevBuf w64, w64t, w32, bias64, cut32, w_tc, cuttc;
 };
 
 struct ErtState {
@@ -578,7 +578,7 @@ int record_detect(bl_ctx* c, const void* in, int pix, int n, long long pitch, lo
     launch_screen(L, P.host, Pd, P.feat32.as<float>(), D.w32.as<float>(), D.cut32.as<float>(),
                   P.cand.as<Candidate>(), P.n_cand.as<unsigned long long>(), P.cand_cap);
   stage_mark(c, BL_STAGE_RESCORE);
-  launch_rescore(L, n, Pd, P.feat64.as<double>(), D.w64.as<double>(), D.bias64.as<double>(), D.thr, D.cell_px,
+  launch_rescore(L, n, Pd, P.feat64.as<double>(), D.w64.as<double>(), D.w64t.as<double>(), D.bias64.as<double>(), D.thr, D.cell_px,
                  P.cand.as<Candidate>(), P.n_cand.as<unsigned long long>(), P.cand_cap, P.dets.as<DevDet>(),
                  P.det_count.as<int>(), P.cap_pf, P.overflow.as<int>());
   stage_mark(c, BL_STAGE_NMS);
@@ -1411,6 +1411,10 @@ int bl_detector_upload(bl_ctx* c, const double* weights, const double* biases, d
   CK(cudaMemcpy(D.w32.p, w32.data(), sizeof(float) * w32.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(D.bias64.p, biases, sizeof(double) * kFilters, cudaMemcpyDefault));
   CK(cudaMemcpy(D.cut32.p, D.cut, sizeof(float) * kFilters, cudaMemcpyHostToDevice));
+  // the small-batch re-score's transposed copy [c][f][r][j] (k_rescore_lat)
+  TRY(D.w64t.ensure(sizeof(double) * kFilters * kFilterW));
+  launch_transpose_weights(Launch{c->own, &c->launches}, D.w64.as<double>(), D.w64t.as<double>());
+  CK(cudaStreamSynchronize(c->own));
   for (Plan& p : c->plans) p.valid = false;
   D.ready = true;
   c->detp = std::move(nd);

@@ -174,8 +174,108 @@ __global__ void __launch_bounds__(32 * kRsWarps) k_rescore(const PlanDesc* __res
   }
 }
 
+// Small batches (a frame or a camera stream's 16): the re-score's time is latency -- a warp's
+// three candidates x 10 window columns of 155 dependent fp64 multiply-adds per lane.  Here a
+// CTA of 64 threads takes one candidate at a time: thread t = r * 10 + j (filter r, window row
+// j) runs its own row chain scratch(r, j) = sum over c, f in the reference's order
+// (detector.cpp:76-88, same as k_rescore), reading the candidate's 10 x 310 features from shared
+// memory (staged with coalesced loads) and the weights from the transposed copy
+// wT[c][f][r][j] (one coalesced 400-B line per step, L1-resident); then the column pass
+// (detector.cpp:91-95).  Bit-identical to k_rescore.
+constexpr int kRlPitch = kRowW + 1;  // 311: smem row pitch of the staged window
+__global__ void __launch_bounds__(64) k_rescore_lat(const PlanDesc* __restrict__ P,
+                                                    const double* __restrict__ feat64,
+                                                    const double* __restrict__ wT,
+                                                    const double* __restrict__ bias, double thr, int cell_px,
+                                                    const Candidate* __restrict__ cand,
+                                                    const unsigned long long* __restrict__ n_cand,
+                                                    long long cand_cap, DevDet* __restrict__ dets,
+                                                    int* __restrict__ det_count, long long cap_pf,
+                                                    int* __restrict__ overflow) {
+  __shared__ double Fs[kWin * kRlPitch];
+  __shared__ double scr[kFilters * kWin];
+  const long long n = min((long long)*n_cand, cand_cap);
+  const int t = threadIdx.x;
+  for (long long i = blockIdx.x; i < n; i += gridDim.x) {
+    const Candidate c = cand[i];
+    const LevelDesc& D = P->lv[c.slot_r >> 8];
+    const double* src = feat64 + (D.cell_off + (long long)c.frame * D.cw * D.ch + (long long)c.cy * D.cw + c.cx) * kFeat;
+    // the window's 10 rows of 10 cells x 31 features: each row is 310 contiguous doubles
+    for (int e = t; e < kWin * kRowW; e += 64) {
+      const int j = e / kRowW, k = e - j * kRowW;
+      Fs[j * kRlPitch + k] = __ldg(src + (long long)j * D.cw * kFeat + k);
+    }
+    __syncthreads();
+    if (t < kFilters * kWin) {
+      const int r = t / kWin, j = t - r * kWin;
+      const double* fr = Fs + j * kRlPitch;
+      const double* wt = wT + t;  // + (c * 31 + f) * 50
+      double acc = 0.0;
+      // weights 31 steps ahead (one window column per batch): the chain waits on fp64 adds,
+      // not on a load per step
+      double wv[kFeat], wn[kFeat];
+#pragma unroll
+      for (int f = 0; f < kFeat; ++f) wv[f] = __ldg(wt + f * (kFilters * kWin));
+#pragma unroll 1
+      for (int c0 = 0; c0 < kRowW; c0 += kFeat) {
+        const int cn = c0 + kFeat < kRowW ? c0 + kFeat : c0;  // next column's weights in flight
+#pragma unroll
+        for (int f = 0; f < kFeat; ++f) wn[f] = __ldg(wt + (cn + f) * (kFilters * kWin));
+#pragma unroll
+        for (int f = 0; f < kFeat; ++f) acc = dadd(acc, dmul(fr[c0 + f], wv[f]));
+#pragma unroll
+        for (int f = 0; f < kFeat; ++f) wv[f] = wn[f];
+      }
+      scr[r * kWin + j] = acc;
+      (void)r;
+    }
+    __syncthreads();
+    if (t < kFilters && ((c.slot_r >> t) & 1)) {
+      double total = 0.0;
+#pragma unroll
+      for (int j = 0; j < kWin; ++j) total = dadd(total, scr[t * kWin + j]);
+      const double sc = dadd(total, bias[t]);
+      if (sc > thr) {  // detector.cpp:110 (strict)
+        DevDet d;
+        d.x = round_half_up(ddiv((double)(c.cx * cell_px), D.c));
+        d.y = round_half_up(ddiv((double)(c.cy * cell_px), D.c));
+        d.w = D.side;
+        d.h = D.side;
+        d.score = sc;
+        d.scale_index = D.level;
+        d.rotation_index = t;
+        const int idx = atomicAdd(det_count + c.frame, 1);
+        if (idx < cap_pf)
+          dets[(long long)c.frame * cap_pf + idx] = d;
+        else
+          atomicExch(overflow, 1);
+      }
+    }
+    __syncthreads();  // Fs / scr reused by the next candidate
+  }
+}
+
+// wT[c][f][r][j] = w[r][j][c][f] (c = window column, f = feature, r = filter, j = window row)
+__global__ void k_transpose_weights(const double* __restrict__ w, double* __restrict__ wT) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= kFilters * kFilterW) return;
+  const int r = e / kFilterW, rem = e - r * kFilterW;
+  const int j = rem / kRowW, cf = rem - j * kRowW;
+  wT[(long long)cf * (kFilters * kWin) + r * kWin + j] = w[e];
+}
+
+void launch_transpose_weights(const Launch& L, const double* w64, double* w64t) {
+  k_transpose_weights<<<(unsigned)div_up(kFilters * kFilterW, 256), 256, 0, L.st>>>(w64, w64t);
+  ++*L.counter;
+}
+
+constexpr int kRsLatFrames = 16;
+#ifndef BL_RS_LAT_GRID
+#define BL_RS_LAT_GRID 4  // CTAs per SM of k_rescore_lat (C2: 25 -> 17 us vs 2)
+#endif  // batches up to this many frames take k_rescore_lat
 constexpr int kRsCtasPerFrame = 8;
 void launch_rescore(const Launch& L, int n_frames, const PlanDesc* Pd, const double* feat64, const double* w64,
+                    const double* w64t,
                     const double* bias, double thr, int cell_px, const Candidate* cand,
                     const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
                     int* det_count, long long cap_pf, int* overflow) {
@@ -185,6 +285,12 @@ void launch_rescore(const Launch& L, int n_frames, const PlanDesc* Pd, const dou
   // persistent: one CTA per SM (the weights fill most of its smem), but a small batch takes
   // fewer: every CTA stages all 124 KB of weights, and for a frame or two that staging, not the
   // few hundred candidates, is the kernel's time (C1: 27 us at 148 CTAs)
+  if (w64t && n_frames <= kRsLatFrames) {
+    k_rescore_lat<<<(unsigned)(sms * BL_RS_LAT_GRID), 64, 0, L.st>>>(Pd, feat64, w64t, bias, thr, cell_px, cand, n_cand, cand_cap,
+                                                       dets, det_count, cap_pf, overflow);
+    ++*L.counter;
+    return;
+  }
   const dim3 grid((unsigned)std::max(1, std::min(sms, n_frames * kRsCtasPerFrame)));
   k_rescore<<<grid, 32 * kRsWarps, kRsSmem, L.st>>>(Pd, feat64, w64, bias, thr, cell_px, cand, n_cand, cand_cap,
                                                     dets, det_count, cap_pf, overflow);

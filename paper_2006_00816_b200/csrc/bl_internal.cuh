@@ -240,6 +240,7 @@ void launch_screen_tc(const Launch& L, const PlanDesc& Ph, const PlanDesc* Pd, c
                       long long cand_cap, float* dbg_scores);
 // bl_exact.cu
 void launch_rescore(const Launch& L, int n_frames, const PlanDesc* Pd, const double* feat64, const double* w64,
+                    const double* w64t /* k_rescore_lat's [c][f][r][j] copy, or null */,
                     const double* bias, double thr, int cell_px, const Candidate* cand,
                     const unsigned long long* n_cand, long long cand_cap, DevDet* dets,
                     int* det_count, long long cap_pf, int* overflow);
@@ -249,6 +250,7 @@ void launch_score_exact_all(const Launch& L, const double* feat64, int cw, int c
                             double bias, double* scores);
 size_t nms_key_bytes();
 long long nms_gkeys_per_frame(long long cap_pf);
+void launch_transpose_weights(const Launch& L, const double* w64, double* w64t);
 void launch_nms(const Launch& L, const DevDet* dets, const int* det_count, long long cap_pf, int n_frames,
                 double iou_thr, DevDet* kept_out, int* kept_count, void* gkeys, long long gkeys_pf);
 void launch_flatten(const Launch& L, const DevDet* kept, const int* kept_count, long long cap_pf,
