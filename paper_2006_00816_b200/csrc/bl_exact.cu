@@ -398,11 +398,13 @@ struct NmsKey {
 static_assert(sizeof(NmsKey) == sizeof(DevDet), "sorted detections reuse the key slots");
 
 // detector.cpp:125-129: score descending, then (y, x, scale_index, rotation_index) ascending.
+// Branch-free (the sort's compare-exchanges are warp-wide: a data-dependent branch chain
+// serialised the lanes); same result as the chain of "if different, compare" tests.
 BL_DEV bool before(const NmsKey& a, const NmsKey& b) {
-  if (a.score != b.score) return a.score > b.score;
-  if (a.t1 != b.t1) return a.t1 < b.t1;
-  if (a.t2 != b.t2) return a.t2 < b.t2;
-  return a.idx < b.idx;
+  const bool sg = a.score > b.score, se = a.score == b.score;
+  const bool t1l = a.t1 < b.t1, t1e = a.t1 == b.t1;
+  const bool t2l = a.t2 < b.t2, t2e = a.t2 == b.t2;
+  return sg | (se & (t1l | (t1e & (t2l | (t2e & (a.idx < b.idx))))));
 }
 
 BL_DEV unsigned long long pack2(int hi, int lo) {
@@ -615,9 +617,17 @@ __global__ void __launch_bounds__(kNmsSmallThreads) k_nms_small(const DevDet* __
           }
         }
       }
-      __syncthreads();
+      // a pass whose partner distance is below 32 stays inside each warp's 32-element slices,
+      // so between two such passes a warp barrier suffices; a pass on either side of the
+      // barrier that crosses warps needs the block barrier
+      const int next_j = j > 1 ? j >> 1 : k;
+      if (j < 32 && next_j < 32)
+        __syncwarp();
+      else
+        __syncthreads();
     }
   }
+  __syncthreads();
   for (int i = tid; i < n; i += blockDim.x) {  // each thread reads its own key before overwriting it
     const int idx = keys[i].idx;
     sorted[i] = D[idx];
@@ -665,19 +675,27 @@ __global__ void __launch_bounds__(kNmsSmallThreads) k_nms_small(const DevDet* __
       if (lane == 0) ovl[a] = m;
     }
     __syncthreads();
-    if (tid == 0) {  // resolve the batch in order; candidates become processed
+    if (warp == 0) {  // resolve the batch in order (a register recurrence over the shuffled
+                      // overlap rows), then every candidate lane marks itself processed and the
+                      // kept ones store themselves at their rank
+      const uint32_t my_ovl = lane < nc ? ovl[lane] : 0u;
       uint32_t keep = 0;
-      int kept = ctl[1];
       for (int a = 0; a < nc; ++a) {
-        if (!(ovl[a] & keep)) {
-          keep |= 1u << a;
-          out[kept++] = sorted[cand[a]];
-        }
-        atomicOr(&supp[cand[a] >> 5], 1u << (cand[a] & 31));
+        const uint32_t oa = __shfl_sync(0xffffffffu, my_ovl, a);
+        if (!(oa & keep)) keep |= 1u << a;
       }
-      ctl[1] = kept;
-      ctl[2] = (int)keep;
-      ctl[3] = cand[nc - 1] + 1;
+      const int kept0 = ctl[1];
+      if (lane < nc) {
+        const int ci = cand[lane];
+        atomicOr(&supp[ci >> 5], 1u << (ci & 31));
+        if ((keep >> lane) & 1u) out[kept0 + __popc(keep & ((1u << lane) - 1u))] = sorted[ci];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        ctl[1] = kept0 + __popc(keep);
+        ctl[2] = (int)keep;
+        ctl[3] = cand[nc - 1] + 1;
+      }
     }
     __syncthreads();
     const uint32_t keep = (uint32_t)ctl[2];
