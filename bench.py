@@ -490,20 +490,23 @@ def measure_configs(args, torch, bl, ctx, stream, det, ert):
     ref = reference()
     cores, _ = host_cpu()
     out = {}
-    steps = max(10, args.steps)
     for name, w, h, b in CONFIGS:
+        # enough batches that the 4-deep pipeline's fill and drain (a batch's full latency at
+        # each end) stay a small fraction of the timed region: ~0.1 s or 40 steps, whichever more
+        steps = max(10, args.steps, int(0.8e9 / (b * w * h)))  # (~8 G px/s: 0.1 s)
         fr = tiled_frames(b, w, h)
         dev = torch.from_numpy(fr).cuda()
-        faces = pipelined(ctx, bl, dev, 4)
+        faces = pipelined(ctx, bl, dev, 20)
         t, _, _ = timed(torch, stream, lambda: pipelined(ctx, bl, dev, steps))
         host = torch.from_numpy(fr).pin_memory().numpy()
-        pipelined(ctx, bl, host, 4)
+        pipelined(ctx, bl, host, 20)
         te, tw, _ = timed(torch, stream, lambda: pipelined(ctx, bl, host, steps))
         st = stage_pass(ctx, bl, dev, 2)
         per, roof = stage_table(st, w, h, b, faces)
         cfps, nsample, dt = cpu_rate(ref, fr, det, ert, cores, budget_s=4.0)
         out[name] = {"workload": f"{w}x{h} x{b} frames per batch, detect + 68 landmarks",
                      "value": round(b * steps / t, 1), "unit": "frames/s", "ms_per_batch": round(t / steps * 1e3, 4),
+                     "batches_timed": steps,
                      "faces_per_batch": faces,
                      "e2e": {"value": round(b * steps / max(te, tw), 1), "unit": "frames/s",
                              "h2d_bytes_per_step": b * w * h, "d2h_bytes_per_step": b * 4 + faces * (32 + 68 * 16)},
