@@ -444,6 +444,9 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
 #ifndef BL_WD_CLOCK
 #define BL_WD_CLOCK 0  // per-phase clock64 totals of face 0, printed (experiments)
 #endif
+#ifndef BL_WD_MINB
+#define BL_WD_MINB 1  // k_ert_wide CTAs per SM the register budget must allow (experiment)
+#endif
 constexpr int kWdMaxThreads = 640;  // 96 registers per thread
 constexpr int kWdInFlight = 16;  // leaf loads in flight per (pair, chunk) thread
 
@@ -458,7 +461,7 @@ int ert_wide_threads(const ErtDev& M) {
 }
 
 template <bool U8>
-__global__ void __launch_bounds__(kWdMaxThreads) k_ert_wide(ErtDev M, const void* __restrict__ frames, int w, int h,
+__global__ void __launch_bounds__(kWdMaxThreads, BL_WD_MINB) k_ert_wide(ErtDev M, const void* __restrict__ frames, int w, int h,
                                                      long long pitch, long long fstride,
                                                      const int* __restrict__ face_frame,
                                                      const int* __restrict__ boxes, int box_stride,
