@@ -208,6 +208,7 @@ struct Slot {
   // at small batches where one cascade fills few SMs, the other slots' cascades
   cudaStream_t est = nullptr;
   bool busy = false;
+  bool eager = false;  // results copied to h_stage with the counts (small batches: one wait)
   int n = 0, w = 0, h = 0, pix = 0, landmarks = 0;
   long long cap_faces = 0;
   uint64_t ticket = 0;
@@ -631,6 +632,7 @@ int check_frames(const void* frames, int pix, int n, int w, int h, size_t pitch,
 // device; n_faces_dev holds the count.  Output landmarks -> c->ert_out.
 // Face-count threshold of the wide (face-per-CTA) cascade, and the per-frame face estimate a
 // streamed batch is judged by before its detections exist (the count stays on the device).
+constexpr size_t kEagerBytes = 2u << 20;  // result areas up to this size come back with the counts
 constexpr long long kErtClusterMaxFaces = 8;  // expected faces up to which the wide cascade runs as 4-CTA clusters
 constexpr long long kErtWideMaxFaces = 400;  // measured crossover 300-600 faces (tools/diag_ert_wide.py)
 constexpr long long kErtFacesPerFrameGuess = 4;
@@ -921,10 +923,21 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
   } else {
     CK(cudaEventRecord(S.ev_done, c->st));
   }
-  // counts + flags back on the slot's D2H stream as soon as compute finishes
+  // counts + flags back on the slot's D2H stream as soon as compute finishes; a small batch's
+  // whole result area follows in the same stream (C1: 2 KB of detections + 70 KB of landmark
+  // rows), so collect waits once instead of a second D2H round trip after the counts arrive
   TRY(ensure_pinned(reinterpret_cast<void*&>(S.h_meta), S.h_meta_cap, sizeof(int) * (n + 4)));
+  const size_t eager_d = sizeof(bl_detection) * (size_t)cap_faces;
+  const size_t eager_l = landmarks ? sizeof(double) * 2 * (*c->ertp).dev.L * (size_t)lm_rows : 0;
+  S.eager = eager_d + eager_l <= kEagerBytes;
+  if (S.eager) TRY(ensure_pinned(S.h_stage, S.h_stage_cap, eager_d + eager_l + 64));  // (slot idle)
   CK(cudaStreamWaitEvent(S.d2h, S.ev_done, 0));
   CK(cudaMemcpyAsync(S.h_meta, meta, sizeof(int) * (n + 3), cudaMemcpyDeviceToHost, S.d2h));
+  if (S.eager) {
+    CK(cudaMemcpyAsync(S.h_stage, S.flat.p, eager_d, cudaMemcpyDeviceToHost, S.d2h));
+    if (eager_l)
+      CK(cudaMemcpyAsync(static_cast<char*>(S.h_stage) + eager_d, S.ert_out.p, eager_l, cudaMemcpyDeviceToHost, S.d2h));
+  }
   CK(cudaEventRecord(S.ev_meta, S.d2h));
   S.busy = true;
   S.n = n;
@@ -971,11 +984,20 @@ int collect(bl_ctx* c, int s, bl_detection* out, int64_t cap, int32_t* counts, i
   const size_t bd = sizeof(bl_detection) * tot;
   const int64_t lm_rows = S.landmarks == BL_LANDMARKS_BEST ? S.n : tot;  // best-only: one row per frame
   const size_t bl = S.landmarks && landmarks ? sizeof(double) * 2 * (*c->ertp).dev.L * lm_rows : 0;
+  if (S.eager) {  // already in the pinned staging area (copied behind the counts)
+    const char* st = static_cast<const char*>(S.h_stage);
+    if (tot > 0 && out) std::memcpy(out, st, bd);
+    if (bl) std::memcpy(landmarks, st + sizeof(bl_detection) * (size_t)S.cap_faces, bl);
+    S.busy = false;
+    return BL_OK;
+  }
   const bool direct_d = !out || is_pinned_or_device(out);
   const bool direct_l = !bl || is_pinned_or_device(landmarks);
   const size_t need = (direct_d ? 0 : bd) + (direct_l ? 0 : bl) + 64;
-  if (S.h_stage_cap < need)  // grow every slot's staging at once (no host allocations mid-pipeline)
-    for (Slot& o : c->slots) TRY(ensure_pinned(o.h_stage, o.h_stage_cap, need + need / 2));
+  if (S.h_stage_cap < need)  // grow every idle slot's staging at once (no host allocations
+                             // mid-pipeline; a busy slot may have a copy in flight into its own)
+    for (Slot& o : c->slots)
+      if (&o == &S || !o.busy) TRY(ensure_pinned(o.h_stage, o.h_stage_cap, need + need / 2));
   char* stage = static_cast<char*>(S.h_stage);
   if (tot > 0 && out)
     CK(cudaMemcpyAsync(direct_d ? (void*)out : stage, S.flat.p, bd, cudaMemcpyDefault, S.d2h));
