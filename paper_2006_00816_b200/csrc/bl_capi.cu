@@ -662,11 +662,12 @@ int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix
   // GPU with kFcFaces-face CTAs (latency), else kFcFaces faces per CTA (leaf-row reuse in L1)
   const bool wide = c->ert_mode == 2 || (c->ert_mode == 0 && expect_faces <= kErtWideMaxFaces);
   if (wide && ert_wide_fits(E.dev)) {
-    // a handful of faces (one frame): a cluster of 4 CTAs per face spreads each level's leaf
-    // rows over four SMs (C1 ERT 0.188 -> 0.169 ms); more faces fill the GPU with one CTA each
+    // a handful of faces (one frame): a cluster of 8 CTAs per face spreads each level's trees
+    // and leaf rows over eight SMs (C1 latency 0.293 ms with 4, 0.280 with 8); more faces fill
+    // the GPU with one CTA each
     launch_ert_wide(L, E.dev, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
                     n_faces_dev, nf, out_xy, leaf_dev, (long long)E.dev.T * E.dev.K, err_dev,
-                    expect_faces <= kErtClusterMaxFaces ? 4 : 1);
+                    expect_faces <= kErtClusterMaxFaces ? 8 : 1);
     return BL_OK;
   }
   if (c->ert_mode != 3 && ert_cascade_fits(E.dev)) {

@@ -613,6 +613,9 @@ __global__ void __launch_bounds__(kWdMaxThreads, BL_WD_MINB) k_ert_wide(ErtDev M
 // transform (warp 0) is computed redundantly and identically in each CTA.  Bit-identical to
 // k_ert_wide.
 constexpr int kWclMax = 8;
+#ifndef BL_ERT_L1PF
+#define BL_ERT_L1PF 0  // prefetch the next level's split records of my trees into L1 (experiment)
+#endif
 #ifndef BL_ERT_SREC
 #define BL_ERT_SREC 0  // split records of the level staged in shared memory (cluster kernel)
 #endif
@@ -820,6 +823,19 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
         asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(rpart[q] + off), "d"(px), "d"(py) : "memory");
     }
     // every chunk's partial is in every CTA (release / acquire across the cluster)
+    if (BL_ERT_L1PF && !srec && t + 1 < M.T) {  // next level's records of my trees into L1
+      const int4* nl = reinterpret_cast<const int4*>(M.split) + (long long)(t + 1) * S * K;
+      const int lines_per = (kLeafChunk * 16) / 128;  // 128-B lines of one (plane, node, chunk) run
+      const int total = my_chunks * 3 * S * lines_per;
+      for (int idx = tid; idx < total; idx += bd) {
+        const int ci = idx / (3 * S * lines_per), rem = idx - ci * 3 * S * lines_per;
+        const int pl = rem / (S * lines_per), rem2 = rem - pl * S * lines_per;
+        const int nd = rem2 / lines_per, li = rem2 - nd * lines_per;
+        const int k0 = ((int)rank + CL * ci) * kLeafChunk;
+        const int4* a = nl + (long long)pl * M.split_plane + (long long)nd * K + k0 + li * 8;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+      }
+    }
     if (srec && t + 1 < M.T) {  // next level's records into the (now free) staging buffer:
       __syncthreads();          // they land during the cluster barrier, the update and the transform
       copy_recs(t + 1);
