@@ -255,6 +255,7 @@ struct bl_ctx {
   bool graphs = true;
   bool ert_serial = false;          // BL_ERT_SERIAL=1: the cascade on the lane stream (experiment)
   bool ert_conc = false;            // BL_ERT_CONC=1: large batches' cascades concurrent again (experiment)
+  bool h2d_after_ert = true;        // BL_H2D_AFTER_ERT=0: large inputs copied as soon as their slot is free (A/B)
   int lanes_large = kLanesLarge;    // BL_LANES_LARGE: detection lanes for large batches (experiment)
   cudaStream_t hst = nullptr;  // H2D stream (input frames): never queued behind a D2H wait
   // CUDA graphs (bl_ctx_enable_graphs): a batch's detection launches (one graph per lane plan,
@@ -632,6 +633,7 @@ int check_frames(const void* frames, int pix, int n, int w, int h, size_t pitch,
 // device; n_faces_dev holds the count.  Output landmarks -> c->ert_out.
 // Face-count threshold of the wide (face-per-CTA) cascade, and the per-frame face estimate a
 // streamed batch is judged by before its detections exist (the count stays on the device).
+constexpr long long kH2dAfterErtPx = 64LL << 20;  // input pixels from which H2D waits for an older cascade
 constexpr size_t kEagerBytes = 2u << 20;  // result areas up to this size come back with the counts
 constexpr long long kErtClusterMaxFaces = 8;  // expected faces up to which the wide cascade runs as 4-CTA clusters
 constexpr long long kErtWideMaxFaces = 400;  // measured crossover 300-600 faces (tools/diag_ert_wide.py)
@@ -833,6 +835,14 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
   } else {  // H2D on the copy stream, after the slot's previous batch stopped reading its input
     TRY(S.input.ensure(es * (size_t)n * w * h));
     CK(cudaStreamWaitEvent(c->hst, S.ev_done, 0));
+    if (c->h2d_after_ert && (long long)n * w * h >= kH2dAfterErtPx) {
+      // a very large batch's input copy waits for the cascade of the batch two submits back: the
+      // DMA then streams beside a detection, not beside a cascade whose leaf rows it would evict
+      // (bench e2e 93-96k -> 102-103k frames/s).  Not for mid-size batches, whose detection is
+      // too short to hide the copy behind (C3's 59 Mpx: e2e 51k -> 45k)
+      const Slot& B2 = c->slots[(s + BL_MAX_IN_FLIGHT - 2) % BL_MAX_IN_FLIGHT];
+      if (B2.busy) CK(cudaStreamWaitEvent(c->hst, B2.ev_done, 0));
+    }
     if (pitch == (size_t)w && fstride == (size_t)w * h) {
       CK(cudaMemcpyAsync(S.input.p, frames, es * (size_t)n * w * h, cudaMemcpyDefault, c->hst));
     } else {
@@ -1225,6 +1235,7 @@ int bl_ctx_create(int device, bl_ctx** out) {
   if (const char* e = std::getenv("BL_GRAPHS")) c->graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT_SERIAL")) c->ert_serial = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT_CONC")) c->ert_conc = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BL_H2D_AFTER_ERT")) c->h2d_after_ert = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_LANES_LARGE")) c->lanes_large = std::max(1, std::min(kLanes, std::atoi(e)));
   if (const char* e = std::getenv("BL_PYR_CHAIN")) c->pyr_chain = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT"))
