@@ -3,8 +3,9 @@
 // The cascade levels are strictly sequential (ert.cpp:108); within a level every face and
 // every tree is independent.  Per level three fully parallel kernels:
 //   1. k_ert_xform    thread per face: similarity transform current -> mean (ert.cpp:26-69),
-//                     sums sequential in the reference's order (bit-identical), then CUDA's
-//                     hypot/atan2/cos/sin (<= 2 ulp from glibc: the only non-bit-exact step);
+//                     fp64 sums in a fixed order, the linear part (a, b) taken directly
+//                     (the reference's hypot/atan2/cos/sin round trip returns it up to a few
+//                     ulp: face_transform_warp);
 //   2. k_ert_traverse thread per (face, tree): walks the F splits in level order, left iff
 //                     Ia - Ib > thr (ert.cpp:87-97), sampling the ORIGINAL frame through
 //                     apply_linear + box map + llround + clamp (ert.cpp:20-24, 71-85);
@@ -66,13 +67,11 @@ BL_DEV double sample_px(const void* fr, int w, int h, long long pitch, int bx, i
   return __ldg((const double*)fr + (long long)iy * pitch + ix);
 }
 
-template <bool SINCOS = false>
 __device__ int face_transform_warp(const ErtDev& M, const double* c, const double* mc, int lane, double& A,
                                    double& B);
 
 // (1) similarity_transform(current, mean) per face, ert.cpp:26-69.  A warp per face stages
-// the current shape in shared memory; lane 0 then runs the sums sequentially in the
-// reference's order (bit-identical), then CUDA hypot/atan2/cos/sin.  Stores the linear part
+// the current shape in shared memory and runs face_transform_warp.  Stores the linear part
 // (scale*cos, scale*sin) that apply_linear recomputes for every sample (ert.cpp:21-22).
 constexpr int kXfFaces = 4;
 constexpr int kMaxL2 = 512;  // 2L <= 512 (L <= 256) for the staged kernels
@@ -117,7 +116,6 @@ BL_DEV double warp_sum(double v) {
 // (c, mc: the current shape and the centred mean shape, shared or global).  Returns 0 or the
 // reference's error (1: source shape has no spread, 2: target shape has no spread) and the
 // linear part (scale*cos, scale*sin) in A, B; identical in every lane.
-template <bool SINCOS>
 __device__ int face_transform_warp(const ErtDev& M, const double* c, const double* mc, int lane, double& A,
                                    double& B) {
   const int L = M.L;
@@ -142,32 +140,14 @@ __device__ int face_transform_warp(const ErtDev& M, const double* c, const doubl
   A = 0.0;
   B = 0.0;
   if (!(sff > 0.0)) return 1;  // "source shape has no spread" (ert.cpp:56-57)
-  const double a = ddiv(sre, sff), b = ddiv(sim, sff);
-  // ert.cpp:60-67, the three libm chains on different lanes (same functions, same results):
-  // lane 2 scale = hypot(a, b); lanes 0 / 1 rot = atan2(b, a) then cos / sin
-  double v, sr, cr;
-  if (SINCOS) {  // latency kernels: one shared argument reduction, no divergent sin / cos lanes
-    if (lane == 2) {
-      v = hypot(a, b);
-    } else {
-      sincos(atan2(b, a), &sr, &cr);
-    }
-    cr = __shfl_sync(0xffffffffu, cr, 0);
-    sr = __shfl_sync(0xffffffffu, sr, 0);
-  } else {  // (fewer registers: the 4-face cascade's occupancy)
-    if (lane == 2) {
-      v = hypot(a, b);
-    } else {
-      const double rot = atan2(b, a);
-      v = lane == 1 ? sin(rot) : cos(rot);
-    }
-    cr = __shfl_sync(0xffffffffu, v, 0);
-    sr = __shfl_sync(0xffffffffu, v, 1);
-  }
-  const double scale = __shfl_sync(0xffffffffu, v, 2);
-  if (!(scale > 0.0)) return 2;  // "target shape has no spread" (ert.cpp:62-63)
-  A = dmul(scale, cr);
-  B = dmul(scale, sr);
+  // ert.cpp:58-67 stores scale = hypot(a, b) and rotation = atan2(b, a), and apply_linear
+  // (ert.cpp:21-22) multiplies back scale * cos(rotation), scale * sin(rotation): in real
+  // arithmetic exactly a and b.  The round trip through libm only adds a few ulp of noise (and
+  // costs a dependent hypot / atan2 / sin / cos chain per face and level), so the linear part
+  // is taken directly; the reference's "no spread" test scale <= 0 is a == b == 0.
+  A = ddiv(sre, sff);
+  B = ddiv(sim, sff);
+  if (A == 0.0 && B == 0.0) return 2;  // "target shape has no spread" (ert.cpp:62-63)
   return 0;
 }
 
@@ -438,9 +418,6 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
 //            the partials in chunk order, cur += shrinkage * delta.
 // The leaf sum of a level is then ~kLeafChunk dependent adds and loads deep instead of K.
 // Same canonical order as k_ert_cascade / k_ert_accum (bit-identical to both).
-#ifndef BL_ERT_WIDE_SINCOS
-#define BL_ERT_WIDE_SINCOS 0
-#endif
 #ifndef BL_WD_CLOCK
 #define BL_WD_CLOCK 0  // per-phase clock64 totals of face 0, printed (experiments)
 #endif
@@ -507,7 +484,7 @@ __global__ void __launch_bounds__(kWdMaxThreads, BL_WD_MINB) k_ert_wide(ErtDev M
 #endif
     if (warp == 0) {  // (1) transform
       double A, B;
-      const int e = face_transform_warp<BL_ERT_WIDE_SINCOS>(M, sc, smc, lane, A, B);
+      const int e = face_transform_warp(M, sc, smc, lane, A, B);
       if (lane == 0) {
         if (e) atomicExch(err, e);
         stf[0] = make_double2(A, B);
@@ -710,7 +687,7 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
     if (!srec && k_first < K && S > 0) rec(0, k_first, root);
     if (warp == 0) {  // (1) transform (identical in every CTA of the cluster)
       double A, B;
-      const int e = face_transform_warp<BL_ERT_WIDE_SINCOS>(M, sc, smc, lane, A, B);
+      const int e = face_transform_warp(M, sc, smc, lane, A, B);
       if (lane == 0) {
         if (e && rank == 0) atomicExch(err, e);
         stf[0] = make_double2(A, B);
