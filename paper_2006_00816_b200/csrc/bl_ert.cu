@@ -590,12 +590,33 @@ __global__ void __launch_bounds__(kWdMaxThreads, BL_WD_MINB) k_ert_wide(ErtDev M
 // transform (warp 0) is computed redundantly and identically in each CTA.  Bit-identical to
 // k_ert_wide.
 constexpr int kWclMax = 8;
-#ifndef BL_ERT_L1PF
-#define BL_ERT_L1PF 0  // prefetch the next level's split records of my trees into L1 (experiment)
-#endif
 #ifndef BL_ERT_SREC
-#define BL_ERT_SREC 0  // split records of the level staged in shared memory (cluster kernel)
+#define BL_ERT_SREC 1  // split records of my trees staged in shared memory one level ahead
 #endif
+
+// shared-memory plan of k_ert_wcl (host and device compute the same offsets)
+struct WclSmem {
+  int my_chunks_max, items_max;
+  bool staged, srec;
+  size_t stage_off, srec_off, total;
+};
+BL_HD_INLINE WclSmem wcl_smem(int L, int K, int S, int CL, int threads) {
+  WclSmem m;
+  const int nchunk = (K + kLeafChunk - 1) / kLeafChunk;
+  m.my_chunks_max = (nchunk + CL - 1) / CL;
+  m.items_max = m.my_chunks_max * L;
+  m.staged = m.items_max <= threads;
+  m.srec = BL_ERT_SREC && m.staged && S > 0;
+  size_t off = sizeof(double) * 4 * (size_t)L + sizeof(double2) * (1 + 2 * (size_t)nchunk * L) + (size_t)((K + kLeafChunk - 1) / kLeafChunk * kLeafChunk);
+  m.stage_off = off;
+  if (m.staged) off += sizeof(double2) * kLeafChunk * (size_t)m.items_max;
+  m.srec_off = off;
+  const size_t recs = sizeof(int4) * 3 * (size_t)S * kLeafChunk * m.my_chunks_max;
+  if (off + recs > 227u * 1024u) m.srec = false;  // the per-CTA shared-memory opt-in limit
+  if (m.srec) off += recs;
+  m.total = off;
+  return m;
+}
 
 template <bool U8, int CL>
 __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restrict__ frames, int w, int h,
@@ -613,12 +634,13 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
   double2* stf = reinterpret_cast<double2*>(smc + L2);         // [1] transform
   double2* spart = stf + 1;                                    // [2][nchunk][L] partial leaf sums (by level parity)
   uint8_t* sli = reinterpret_cast<uint8_t*>(spart + 2 * nchunk * L);  // [K]
-  // [kLeafChunk][items] leaf pairs of this CTA's items, landed by cp.async (16-B aligned)
-  double2* stage = reinterpret_cast<double2*>(sli + ((K + 15) & ~15));
-  // the level's split records of my trees, [3 planes][S][my trees], share the staging
-  // buffer (records live during the traversal, leaf pairs during the accumulation)
-  int4* srecs = reinterpret_cast<int4*>(stage);
   const int bd = blockDim.x;
+  const WclSmem plan = wcl_smem(L, K, S, CL, bd);
+  // [kLeafChunk][items] leaf pairs of this CTA's items, landed by cp.async (16-B aligned)
+  double2* stage = reinterpret_cast<double2*>(wd_smem + plan.stage_off);
+  // the next level's split records of my trees, [3 planes][S][my trees] (cp.async, landed
+  // during this level's accumulation, cluster barrier and transform)
+  int4* srecs = reinterpret_cast<int4*>(wd_smem + plan.srec_off);
   const int n = min(*n_faces, cap);
   const int face = blockIdx.x / CL;
   const unsigned rank = blockIdx.x % CL;  // == %cluster_ctarank for cluster dims (CL, 1, 1)
@@ -634,7 +656,7 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
   // my chunks: rank, rank + CL, ...; my trees: kLeafChunk per chunk
   const int my_chunks = nchunk > (int)rank ? (nchunk - 1 - (int)rank) / CL + 1 : 0;
   const int my_trees = my_chunks * kLeafChunk;
-  const bool srec = BL_ERT_SREC && my_chunks * L <= bd && 3 * S * my_trees * 16 <= kLeafChunk * my_chunks * L * 16;
+  const bool srec = plan.srec;
   auto tree_of = [&](int lt) { return (int)(rank + CL * (lt / kLeafChunk)) * kLeafChunk + lt % kLeafChunk; };
   // DSMEM base addresses of spart in every CTA of the cluster
   uint32_t rpart[CL];
@@ -647,22 +669,22 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
   // level t's split records of my trees -> srecs (cp.async, one commit group)
   auto copy_recs = [&](int t) {
     const int4* src = reinterpret_cast<const int4*>(M.split) + (long long)t * S * K;
-    const int per_plane = S * my_trees;
-    for (int idx = tid; idx < 3 * per_plane; idx += bd) {
-      const int pl = idx / per_plane, rem = idx - pl * per_plane;
-      const int nd = rem / my_trees, lt = rem - nd * my_trees;
+    for (int lt = tid; lt < my_trees; lt += bd) {
       const int k = tree_of(lt);
-      if (k < K)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(srecs + idx)),
-                     "l"(src + (long long)pl * M.split_plane + (long long)nd * K + k)
-                     : "memory");
+      if (k >= K) continue;
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(srecs + lt);
+      for (int pl = 0; pl < 3; ++pl)
+        for (int nd = 0; nd < S; ++nd)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + (uint32_t)((pl * S + nd) * my_trees * 16)),
+                       "l"(src + (long long)pl * M.split_plane + (long long)nd * K + k)
+                       : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   if (srec && my_chunks > 0) copy_recs(0);
   __syncthreads();
 #if BL_WD_CLOCK
-  long long clk[4] = {0, 0, 0, 0};
+  long long clk[7] = {0, 0, 0, 0, 0, 0, 0};
 #endif
   for (int t = 0; t < M.T; ++t) {
 #if BL_WD_CLOCK
@@ -706,9 +728,20 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
       int node = 0;
       SplitPlanes r;
       const int jl = lt;
-      if (srec)
-        rec_s(0, jl, r);
-      else if (lt == tid)
+      if (srec) {  // records in shared memory: no prefetch of the children needed
+        for (int d = 0; d < M.F; ++d) {
+          rec_s(node, jl, r);
+          const double thr = __hiloint2double(r.tail.y, r.tail.x);
+          const int an_a = (short)(r.tail.z & 0xffff), an_b = (short)(r.tail.z >> 16);
+          const double ia = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_a, r.oa.x, r.oa.y);
+          const double ib = sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an_b, r.ob.x, r.ob.y);
+          node = dsub(ia, ib) > thr ? 2 * node + 1 : 2 * node + 2;
+        }
+        sli[k] = (uint8_t)(node - S);
+        if (leaf_out) leaf_out[(long long)face * leaf_out_stride + (long long)t * K + k] = (uint8_t)(node - S);
+        continue;
+      }
+      if (lt == tid)
         r = root;
       else
         rec(0, k, r);
@@ -716,13 +749,8 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
         SplitPlanes c1, c2;
         const bool more = d + 1 < M.F;
         if (more) {
-          if (srec) {
-            rec_s(2 * node + 1, jl, c1);
-            rec_s(2 * node + 2, jl, c2);
-          } else {
-            rec(2 * node + 1, k, c1);
-            rec(2 * node + 2, k, c2);
-          }
+          rec(2 * node + 1, k, c1);
+          rec(2 * node + 2, k, c2);
         }
         const double thr = __hiloint2double(r.tail.y, r.tail.x);
         const int an_a = (short)(r.tail.z & 0xffff), an_b = (short)(r.tail.z >> 16);
@@ -753,29 +781,54 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
         // every selected leaf pair of the chunk in flight at once: cp.async into this item's
         // column of the staging buffer ([tree][item]: conflict-free), one wait, then the
         // tree-ordered sum from shared memory -- one L2 round trip instead of K/16
+        // (lean: 32-bit offsets, running pointers, no per-tree predicates -- the kernel runs
+        // 3 warps per SM, so its level time is mostly instruction issue)
+        const uint32_t istride = (uint32_t)items * 16u;
         const uint32_t st0 = (uint32_t)__cvta_generic_to_shared(stage + it);
-        for (int kb = k0; kb < k1; kb += 16) {  // 16 trees per step: one 16-B read of their leaf indices
-          const uint4 li4 = *reinterpret_cast<const uint4*>(sli + kb);
-          const uint32_t lw[4] = {li4.x, li4.y, li4.z, li4.w};
+        const int nk = k1 - k0;
+        {
+          // the chunk's leaf indices into registers first: an LDS after an LDGSTS waits for
+          // it (possible aliasing), which serialised the issue loop at ~60 cycles per tree
+          uint32_t lw[kLeafChunk / 4];
 #pragma unroll
-          for (int u = 0; u < 16; ++u)
-            if (kb + u < k1)
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st0 + (uint32_t)((kb + u - k0) * items * 16)),
-                           "l"(lv + (long long)(kb + u) * row + (int)((lw[u >> 2] >> (8 * (u & 3))) & 0xffu) * L + p)
-                           : "memory");
+          for (int q = 0; q < kLeafChunk / 16; ++q) {
+            const uint4 v = *reinterpret_cast<const uint4*>(sli + k0 + 16 * q);
+            lw[4 * q] = v.x;
+            lw[4 * q + 1] = v.y;
+            lw[4 * q + 2] = v.z;
+            lw[4 * q + 3] = v.w;
+          }
+          const double2* src = lv + (long long)k0 * row + p;
+          uint32_t dst = st0;
+          int roff = 0;
+#pragma unroll
+          for (int j = 0; j < kLeafChunk; ++j) {
+            if (j < nk)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                           "l"(src + (roff + (int)((lw[j >> 2] >> (8 * (j & 3))) & 0xffu) * L)));
+            dst += istride;
+            roff += row;
+          }
+#if BL_WD_CLOCK
+          const long long ca = clock64();
+#endif
+          asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+#if BL_WD_CLOCK
+          const long long cb = clock64();
+          if (tid == 0) { clk[4] += ca - c2; clk[5] += cb - ca; }
+#endif
         }
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-        for (int kb = k0; kb < k1; kb += 16) {
-          double2 v[16];
-#pragma unroll
-          for (int u = 0; u < 16; ++u) v[u] = kb + u < k1 ? stage[(kb + u - k0) * items + it] : make_double2(0.0, 0.0);
-#pragma unroll
-          for (int u = 0; u < 16; ++u)
-            if (kb + u < k1) {
-              px = dadd(px, v[u].x);
-              py = dadd(py, v[u].y);
-            }
+        const double2* sp = stage + it;
+#pragma unroll 16
+        for (int j = 0; j < nk; ++j) {
+          const double2 v = *sp;
+          px = dadd(px, v.x);
+          py = dadd(py, v.y);
+          sp += items;
         }
+#if BL_WD_CLOCK
+        if (tid == 0) clk[6] -= clock64();
+#endif
       } else {
         int k = k0;
         for (; k + kWdInFlight <= k1; k += kWdInFlight) {
@@ -798,25 +851,12 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
 #pragma unroll
       for (int q = 0; q < CL; ++q)
         asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(rpart[q] + off), "d"(px), "d"(py) : "memory");
+#if BL_WD_CLOCK
+      if (tid == 0) clk[6] += clock64();
+#endif
     }
     // every chunk's partial is in every CTA (release / acquire across the cluster)
-    if (BL_ERT_L1PF && !srec && t + 1 < M.T) {  // next level's records of my trees into L1
-      const int4* nl = reinterpret_cast<const int4*>(M.split) + (long long)(t + 1) * S * K;
-      const int lines_per = (kLeafChunk * 16) / 128;  // 128-B lines of one (plane, node, chunk) run
-      const int total = my_chunks * 3 * S * lines_per;
-      for (int idx = tid; idx < total; idx += bd) {
-        const int ci = idx / (3 * S * lines_per), rem = idx - ci * 3 * S * lines_per;
-        const int pl = rem / (S * lines_per), rem2 = rem - pl * S * lines_per;
-        const int nd = rem2 / lines_per, li = rem2 - nd * lines_per;
-        const int k0 = ((int)rank + CL * ci) * kLeafChunk;
-        const int4* a = nl + (long long)pl * M.split_plane + (long long)nd * K + k0 + li * 8;
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
-      }
-    }
-    if (srec && t + 1 < M.T) {  // next level's records into the (now free) staging buffer:
-      __syncthreads();          // they land during the cluster barrier, the update and the transform
-      copy_recs(t + 1);
-    }
+    if (srec && t + 1 < M.T) copy_recs(t + 1);  // lands during the barrier, update and transform
 #if BL_WD_CLOCK
     const long long c3 = clock64();
 #endif
@@ -846,8 +886,8 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
   }
 #if BL_WD_CLOCK
   if (tid == 0 && face == 0)
-    printf("k_ert_wcl face 0 rank %u cycles: xform %lld traverse %lld accum %lld cluster-sync %lld\n", rank, clk[0],
-           clk[1], clk[2], clk[3]);
+    printf("k_ert_wcl face 0 rank %u cycles: xform %lld traverse %lld accum %lld (issue %lld wait %lld bcast %lld) cluster-sync %lld\n", rank, clk[0],
+           clk[1], clk[2], clk[4], clk[5], clk[6], clk[3]);
 #endif
   // no CTA may exit while another could still write into its shared memory: every remote
   // write of the last level precedes the last cluster barrier, so exiting is safe here
@@ -865,10 +905,7 @@ static cudaError_t launch_wcl(const Launch& L, const ErtDev& M, const void* fram
   const int nchunk = (int)div_up(M.K, kLeafChunk);
   const int my_chunks = (nchunk + CL - 1) / CL;
   const int threads = (int)std::min<long long>(256, div_up(std::max(my_chunks * std::max(kLeafChunk, M.L), 32), 32) * 32);
-  const size_t items = (size_t)my_chunks * M.L;
-  size_t smem = sizeof(double) * 4 * M.L + sizeof(double2) * (1 + 2 * (size_t)nchunk * M.L) + (size_t)((M.K + 15) & ~15);
-  if ((int)items <= threads) smem += sizeof(double2) * kLeafChunk * items;  // cp.async staging
-  // (the split records of a level share the staging buffer when they fit, see k_ert_wcl)
+  const size_t smem = wcl_smem(M.L, M.K, M.S, CL, threads).total;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cap * CL);
   cfg.blockDim = dim3(threads);
