@@ -281,6 +281,10 @@ struct TravItem {  // one (face, tree) traversal in flight
 #endif
 constexpr int kFcFaces = BL_ERT_FACES;
 constexpr int kFcThreads = ((kFcFaces * 68 + 31) / 32) * 32;  // one thread per (face, pair) at L = 68
+#ifndef BL_FC_LEAN
+#define BL_FC_LEAN 1  // k_ert_cascade leaf sums: 16 leaf indices per 16-B shared load (not 16 LDS.U8)
+#endif
+BL_HD_INLINE int fc_sli_stride(int K) { return (K + 15) & ~15; }  // per-face leaf indices, 16-B rows
 
 template <bool U8>
 __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void* __restrict__ frames, int w, int h,
@@ -294,7 +298,8 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
   const int L = M.L, L2 = 2 * L, K = M.K, S = M.S, NL = M.NL;
   double* sc = reinterpret_cast<double*>(fc_smem);                    // [kFcFaces][2L]
   double2* stf = reinterpret_cast<double2*>(sc + kFcFaces * L2);      // [kFcFaces]
-  uint8_t* sli = reinterpret_cast<uint8_t*>(stf + kFcFaces);          // [kFcFaces][K]
+  uint8_t* sli = reinterpret_cast<uint8_t*>(stf + kFcFaces);          // [kFcFaces][Kp]
+  const int Kp = fc_sli_stride(K);
   const int n = min(*n_faces, cap);
   const int f0 = blockIdx.x * kFcFaces;
   if (f0 >= n) return;
@@ -356,7 +361,7 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int leaf = it[q].node - S;
-        sli[it[q].fi * K + it[q].k] = (uint8_t)leaf;
+        sli[it[q].fi * Kp + it[q].k] = (uint8_t)leaf;
         if (leaf_out)
           leaf_out[(long long)(f0 + it[q].fi) * leaf_out_stride + (long long)t * K + it[q].k] = (uint8_t)leaf;
       }
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
     if (BL_ERT_EVICT_LAST) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     if (tid < nf * L) {
       const int fi = tid / L, p = tid - fi * L;
-      const uint8_t* li = sli + fi * K;
+      const uint8_t* li = sli + fi * Kp;
       const double2* lv = reinterpret_cast<const double2*>(M.leaves + (long long)t * K * NL * 2 * L) + p;
       const int row = NL * L;
       double ax = 0.0, ay = 0.0;  // the canonical chunked order
@@ -377,8 +382,16 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
         int k = c0;
         for (; k + 16 <= c1; k += 16) {
           double2 v[16];
+#if BL_FC_LEAN
+          const uint4 li4 = *reinterpret_cast<const uint4*>(li + k);
+          const uint32_t lw[4] = {li4.x, li4.y, li4.z, li4.w};
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            v[u] = ld_leaf(lv + (k + u) * row + (int)((lw[u >> 2] >> (8 * (u & 3))) & 0xffu) * L, pol);
+#else
 #pragma unroll
           for (int u = 0; u < 16; ++u) v[u] = ld_leaf(lv + (k + u) * row + li[k + u] * L, pol);
+#endif
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             px = dadd(px, v[u].x);
@@ -420,6 +433,9 @@ __global__ void __launch_bounds__(kFcThreads) k_ert_cascade(ErtDev M, const void
 // Same canonical order as k_ert_cascade / k_ert_accum (bit-identical to both).
 #ifndef BL_WD_CLOCK
 #define BL_WD_CLOCK 0  // per-phase clock64 totals of face 0, printed (experiments)
+#endif
+#ifndef BL_WD_LEAN
+#define BL_WD_LEAN 1  // k_ert_wide: 16-B leaf-index loads and 32-bit row offsets in the leaf sums
 #endif
 #ifndef BL_WD_MINB
 #define BL_WD_MINB 1  // k_ert_wide CTAs per SM the register budget must allow (experiment)
@@ -536,6 +552,23 @@ __global__ void __launch_bounds__(kWdMaxThreads, BL_WD_MINB) k_ert_wide(ErtDev M
       const int k0 = ch * kLeafChunk, k1 = min(K, k0 + kLeafChunk);
       double px = 0.0, py = 0.0;
       int k = k0;
+#if BL_WD_LEAN
+      // 16 leaf indices per 16-B shared load, 32-bit row offsets from the chunk's base
+      const double2* src = lv + (long long)k0 * row + p;
+      for (int qrow = 0; k + kWdInFlight <= k1; k += kWdInFlight, qrow += kWdInFlight * row) {
+        const uint4 li4 = *reinterpret_cast<const uint4*>(sli + k);
+        const uint32_t lw[4] = {li4.x, li4.y, li4.z, li4.w};
+        double2 v[kWdInFlight];
+#pragma unroll
+        for (int u = 0; u < kWdInFlight; ++u)
+          v[u] = __ldg(src + (qrow + u * row + (int)((lw[u >> 2] >> (8 * (u & 3))) & 0xffu) * L));
+#pragma unroll
+        for (int u = 0; u < kWdInFlight; ++u) {
+          px = dadd(px, v[u].x);
+          py = dadd(py, v[u].y);
+        }
+      }
+#endif
       for (; k + kWdInFlight <= k1; k += kWdInFlight) {
         double2 v[kWdInFlight];
 #pragma unroll
@@ -969,7 +1002,8 @@ void launch_ert_cascade(const Launch& L, const ErtDev& M, const void* frames, in
                         long long fstride, const int* face_frame, const int* boxes, int box_stride,
                         const int* n_faces, int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride,
                         int* err) {
-  const size_t smem = sizeof(double) * kFcFaces * 2 * M.L + sizeof(double2) * kFcFaces + (size_t)kFcFaces * M.K;
+  const size_t smem =
+      sizeof(double) * kFcFaces * 2 * M.L + sizeof(double2) * kFcFaces + (size_t)kFcFaces * fc_sli_stride(M.K);
   const unsigned grid = (unsigned)div_up(cap, kFcFaces);
   if (u8)
     k_ert_cascade<true><<<grid, kFcThreads, smem, L.st>>>(M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride,
