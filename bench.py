@@ -545,33 +545,45 @@ def measure_configs(args, torch, bl, ctx, stream, det, ert):
     return out
 
 
-def measure_run(bl, ctx, det, ert, ref, cores, n=256, batch=64):
+def measure_run(bl, ctx, det, ert, ref, cores, n=1024, n_ref=256, batch=64, repeats=3):
     """run() end to end (pipeline.cpp:396-404): a directory of n 640x480 PGM frames -> decode,
     detect, the best face's 68 landmarks, EAR trace.  Ours: bl_run (persistent decoder thread
-    into pinned buffers, BL_MAX_IN_FLIGHT batches in flight); reference: its pipelined run()
-    with all usable host threads as workers.  Wall clock, PGM decode included on both sides."""
+    into pinned buffers, BL_MAX_IN_FLIGHT batches in flight) over n frames, the median of
+    `repeats` timed runs (a 256-frame run is dominated by start-up: 1.3-2.7k frames/s against
+    6-9.5k over 1024); reference: its pipelined run() with all usable host threads as workers
+    over the first n_ref frames (a bounded sample; its rate is compute-bound and flat).  Wall
+    clock, PGM decode included on both sides; the first n_ref frames' results are compared."""
     import shutil
     import tempfile
     d = tempfile.mkdtemp(prefix="bl_run_")
+    dr = tempfile.mkdtemp(prefix="bl_run_ref_")
     try:
         for i, f in enumerate(tiled_frames(n, W, H, distinct=32, seed=91)):
             bl.write_pgm(os.path.join(d, f"frame_{i:06d}.pgm"), f)
+            if i < n_ref:
+                bl.write_pgm(os.path.join(dr, f"frame_{i:06d}.pgm"), f)
         ctx.run(d, 30.0, batch_size=batch)  # warm-up (plans, graphs, page cache)
+        times = []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            ours = ctx.run(d, 30.0, batch_size=batch)
+            times.append(time.perf_counter() - t0)
+        t_ours = float(np.median(times))
+        ref.run(dr, det, ert, 30.0, pipelined=cores, batch_size=16)  # warm-up
         t0 = time.perf_counter()
-        ours = ctx.run(d, 30.0, batch_size=batch)
-        t_ours = time.perf_counter() - t0
-        ref.run(d, det, ert, 30.0, pipelined=cores, batch_size=16)  # warm-up
-        t0 = time.perf_counter()
-        want = ref.run(d, det, ert, 30.0, pipelined=cores, batch_size=16)
+        want = ref.run(dr, det, ert, 30.0, pipelined=cores, batch_size=16)
         t_ref = time.perf_counter() - t0
-        same = bool(np.array_equal(ours["detections"], want["detections"]) and
-                    np.array_equal(ours["frames"]["face_found"], want["face_found"]))
+        nd = int(np.sum(ours["frames"]["n_detections"][:n_ref]))
+        same = bool(np.array_equal(ours["detections"][:nd], want["detections"]) and
+                    np.array_equal(ours["frames"]["face_found"][:n_ref], want["face_found"]))
     finally:
         shutil.rmtree(d, ignore_errors=True)
+        shutil.rmtree(dr, ignore_errors=True)
     return {"workload": f"run(): {n} PGM frames {W}x{H}, decode + detect + best-face landmarks + EAR trace",
             "value": round(n / t_ours, 1), "unit": "frames/s", "batch_size": batch,
-            "reference": {"value": round(n / t_ref, 2), "unit": "frames/s", "workers": cores,
-                          "kind": "reference run(), pipelined"},
+            "timing": f"median of {repeats} runs over {n} frames",
+            "reference": {"value": round(n_ref / t_ref, 2), "unit": "frames/s", "workers": cores,
+                          "kind": "reference run(), pipelined", "sample_frames": n_ref},
             "detections_identical": same}
 
 

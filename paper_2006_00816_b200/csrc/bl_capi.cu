@@ -283,6 +283,7 @@ struct bl_ctx {
   // landmark cascade kernel: auto (k_ert_wide for small batches, else k_ert_cascade), or forced
   // by BL_ERT=wide|cascade|levels (experiments)
   int ert_mode = 0;
+  int ert_cl = 0;  // BL_ERT_CL=1|2|4|8: forces the small-batch cascade's cluster size (A/B, tests)
   bool pyr_fuse = true;  // fused resample pairs over unscored levels (BL_PYR_FUSE=0 disables)
   bool pyr_chain = true;  // one cooperative launch for a small batch's chain (BL_PYR_CHAIN=0 disables)
 };
@@ -669,7 +670,7 @@ int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix
     // the GPU with one CTA each
     launch_ert_wide(L, E.dev, frames, pix == BL_PIX_U8, w, h, pitch, fstride, face_frame, boxes, box_stride,
                     n_faces_dev, nf, out_xy, leaf_dev, (long long)E.dev.T * E.dev.K, err_dev,
-                    expect_faces <= kErtClusterMaxFaces ? 8 : 1);
+                    c->ert_cl ? c->ert_cl : (expect_faces <= kErtClusterMaxFaces ? 8 : 1));
     return BL_OK;
   }
   if (c->ert_mode != 3 && ert_cascade_fits(E.dev)) {
@@ -1236,6 +1237,7 @@ int bl_ctx_create(int device, bl_ctx** out) {
   if (const char* e = std::getenv("BL_ERT_SERIAL")) c->ert_serial = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT_CONC")) c->ert_conc = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_H2D_AFTER_ERT")) c->h2d_after_ert = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BL_ERT_CL")) c->ert_cl = std::atoi(e);
   if (const char* e = std::getenv("BL_LANES_LARGE")) c->lanes_large = std::max(1, std::min(kLanes, std::atoi(e)));
   if (const char* e = std::getenv("BL_PYR_CHAIN")) c->pyr_chain = std::atoi(e) != 0;
   if (const char* e = std::getenv("BL_ERT"))

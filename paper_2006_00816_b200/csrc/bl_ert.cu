@@ -960,11 +960,7 @@ bool ert_wide_fits(const ErtDev& M) { return 2 * M.L <= kMaxL2; }
 void launch_ert_wide(const Launch& L, const ErtDev& M, const void* frames, int u8, int w, int h, long long pitch,
                      long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces,
                      int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err, int cl_req) {
-  static const int cl_env = [] {  // BL_ERT_CL=1|2|4|8 forces the cluster size (A/B)
-    const char* e = std::getenv("BL_ERT_CL");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int cl = cl_env ? cl_env : cl_req;
+  const int cl = cl_req;  // 1: one CTA per face; 2, 4, 8: a cluster of that many CTAs per face
   if (cl == 2 || cl == 4 || cl == 8) {
     cudaError_t r = cudaSuccess;
     if (cl == 2)

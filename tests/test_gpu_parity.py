@@ -1,7 +1,7 @@
 """Per-stage parity of the CUDA path against the CPU oracle (and the reference's golden
 vectors), through the C-ABI.  Bar: bit-exact for every stage the reference defines to the last
-bit; ERT landmarks within 1e-9 px (the only libm-dependent step is the similarity transform's
-hypot/atan2/cos/sin), leaf indices exact.
+bit; ERT landmarks within 1e-9 px (the only non-bit-exact step is the similarity transform's
+linear part, taken directly instead of through hypot/atan2/cos/sin), leaf indices exact.
 
 Reference tests restated here: test_image.cpp (bilinear, pyramid dims), test_hog.cpp (ramp,
 border ring, atan2 oracle, single-pixel split, mass conservation, all-ones energy, feature
@@ -385,6 +385,37 @@ def test_ert_wide_and_cascade_kernels_agree(monkeypatch, oracle, n):
         wxy, wl, _ = oracle.predict_landmarks(img, tuple(boxes[i]), ert)
         assert np.array_equal(out["wide"][1][i], wl)
         assert np.max(np.abs(out["wide"][0][i] - wxy)) <= 1e-9
+
+
+@pytest.mark.parametrize("K", [40, 300, 500])
+def test_ert_cluster_sizes_agree(monkeypatch, oracle, K):
+    """The small-batch cascade as clusters of 2, 4 and 8 CTAs per face (k_ert_wcl: chunks
+    spread over the cluster, partials broadcast through DSMEM; 2 = unstaged sums, 4 = two
+    chunks per CTA, 8 = one chunk per CTA and ranks without a chunk when K <= 448) is
+    bit-identical to the one-CTA kernel and matches the oracle's leaves and landmarks."""
+    import paper_2006_00816_b200 as bl
+    from pyoracle import random_ert
+    ert = random_ert(T=3, K=K, F=4, seed=21)
+    img = np.floor(rng(22).uniform(0, 256, (240, 320)))
+    r = rng(23)
+    n = 5
+    boxes = np.stack([r.integers(-20, 260, n), r.integers(-20, 180, n), r.integers(30, 160, n),
+                      r.integers(30, 160, n)], axis=1).astype(np.int32)
+    out = {}
+    for cl in (1, 2, 4, 8):
+        monkeypatch.setenv("BL_ERT", "wide")
+        monkeypatch.setenv("BL_ERT_CL", str(cl))
+        c = bl.Context(0)
+        c.upload_ert(ert)
+        out[cl] = c.landmarks(img.astype(np.uint8), np.zeros(n, np.int32), boxes, want_leaves=True)
+        c.close()
+    for cl in (2, 4, 8):
+        assert np.array_equal(out[cl][0], out[1][0]), cl
+        assert np.array_equal(out[cl][1], out[1][1]), cl
+    for i in range(n):
+        wxy, wl, _ = oracle.predict_landmarks(img, tuple(boxes[i]), ert)
+        assert np.array_equal(out[8][1][i], wl)
+        assert np.max(np.abs(out[8][0][i] - wxy)) <= 1e-9
 
 
 def test_ert_zero_delta_is_mean_shape(ctx):
