@@ -12,6 +12,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "bl_internal.cuh"
 
@@ -285,6 +286,9 @@ void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int s
 // by ONE cooperative launch, a grid-stride pass per level with a grid barrier between levels
 // (level k reads level k-1).  Per pixel the same arithmetic as k_resample (bit-identical).
 namespace cg = cooperative_groups;
+#ifndef BL_PYR_CHAIN_CTAS_DEFAULT
+#define BL_PYR_CHAIN_CTAS_DEFAULT 2  // C1 chain 25.0 (1) -> 22.1 (2) -> 25.7 us (4)
+#endif
 
 template <typename T0>
 __global__ void __launch_bounds__(256) k_pyramid_chain(const PyrChain C) {
@@ -294,11 +298,13 @@ __global__ void __launch_bounds__(256) k_pyramid_chain(const PyrChain C) {
     const int sw = C.lw[k - 1], sh = C.lh[k - 1], dw = C.lw[k], dh = C.lh[k];
     const double rx = C.rx[k], ry = C.ry[k];
     const double xmax = (double)(sw - 1), ymax = (double)(sh - 1);
-    const long long total = (long long)C.n_frames * dh * dw;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-      const int f = (int)(i / ((long long)dh * dw));
-      const int rem = (int)(i - (long long)f * dh * dw);
-      const int y = rem / dw, x = rem - (rem / dw) * dw;
+    // 32-bit index math (a one-frame pyramid is < 2^31 pixels per level; kChainMaxPx): the
+    // 64-bit division per pixel was a software routine
+    const unsigned plane = (unsigned)dh * (unsigned)dw, total = (unsigned)C.n_frames * plane;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (unsigned)stride) {
+      const unsigned f = C.n_frames == 1 ? 0u : i / plane;
+      const unsigned rem = i - f * plane;
+      const int y = (int)(rem / (unsigned)dw), x = (int)(rem - (unsigned)y * (unsigned)dw);
       double sx = dsub(dmul(dadd((double)x, 0.5), rx), 0.5);  // image.cpp:139-149
       sx = sx < 0.0 ? 0.0 : (xmax < sx ? xmax : sx);
       const int x0 = (int)sx, x1 = min(x0 + 1, sw - 1);
@@ -338,8 +344,12 @@ int launch_pyramid_chain(const Launch& L, const PyrChain& C, int src_u8) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
   long long most = 0;  // the largest level's pixels: no more CTAs than it needs
   for (int k = 1; k < C.n_levels; ++k) most = std::max(most, (long long)C.n_frames * C.lw[k] * C.lh[k]);
-  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((long long)sms * std::min(per_sm, 1),
-                                                                               div_up(most, 256)));
+  static const int cap_per_sm = [] {  // BL_PYR_CHAIN_CTAS: co-resident CTAs per SM (A/B)
+    const char* e = std::getenv("BL_PYR_CHAIN_CTAS");
+    return e ? std::max(1, std::atoi(e)) : BL_PYR_CHAIN_CTAS_DEFAULT;
+  }();
+  const unsigned grid = (unsigned)std::max<long long>(
+      1, std::min<long long>((long long)sms * std::min(per_sm, cap_per_sm), div_up(most, 256)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(256);
