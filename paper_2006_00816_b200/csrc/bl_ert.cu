@@ -699,10 +699,12 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
     for (int q = 0; q < CL; ++q)
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rpart[q]) : "r"(local), "r"(q));
   }
-  // level t's split records of my trees -> srecs (cp.async, one commit group)
-  auto copy_recs = [&](int t) {
+  // level t's split records of my trees -> srecs (cp.async, one commit group), issued by
+  // threads [t0, bd) while warp 0 computes the level's transform: they land before the
+  // traversal needs them, off the level's critical path
+  auto copy_recs = [&](int t, int t0) {
     const int4* src = reinterpret_cast<const int4*>(M.split) + (long long)t * S * K;
-    for (int lt = tid; lt < my_trees; lt += bd) {
+    for (int lt = tid - t0; lt < my_trees; lt += bd - t0) {
       const int k = tree_of(lt);
       if (k >= K) continue;
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(srecs + lt);
@@ -714,7 +716,6 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  if (srec && my_chunks > 0) copy_recs(0);
   __syncthreads();
 #if BL_WD_CLOCK
   long long clk[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -740,6 +741,7 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
     SplitPlanes root;
     const int k_first = tid < my_trees ? tree_of(tid) : K;
     if (!srec && k_first < K && S > 0) rec(0, k_first, root);
+    if (srec && (bd == 32 || warp > 0)) copy_recs(t, bd == 32 ? 0 : 32);
     if (warp == 0) {  // (1) transform (identical in every CTA of the cluster)
       double A, B;
       const int e = face_transform_warp(M, sc, smc, lane, A, B);
@@ -889,7 +891,6 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
 #endif
     }
     // every chunk's partial is in every CTA (release / acquire across the cluster)
-    if (srec && t + 1 < M.T) copy_recs(t + 1);  // lands during the barrier, update and transform
 #if BL_WD_CLOCK
     const long long c3 = clock64();
 #endif
