@@ -623,6 +623,10 @@ __global__ void __launch_bounds__(kWdMaxThreads, BL_WD_MINB) k_ert_wide(ErtDev M
 // transform (warp 0) is computed redundantly and identically in each CTA.  Bit-identical to
 // k_ert_wide.
 constexpr int kWclMax = 8;
+#ifndef BL_ERT_SPEC2
+#define BL_ERT_SPEC2 1  // k_ert_wcl traversal: two depths per pixel round trip (speculative children;
+                        // all 15 nodes at once measured slower: C1 0.289 vs 0.216 ms, stack use)
+#endif
 #ifndef BL_ERT_SREC
 #define BL_ERT_SREC 1  // split records of my trees staged in shared memory one level ahead
 #endif
@@ -764,7 +768,30 @@ __global__ void __launch_bounds__(256) k_ert_wcl(ErtDev M, const void* __restric
       SplitPlanes r;
       const int jl = lt;
       if (srec) {  // records in shared memory: no prefetch of the children needed
-        for (int d = 0; d < M.F; ++d) {
+        // two depths per step: the node's and both children's pixels are sampled together
+        // (6 loads in flight), then both decisions are taken -- one pixel round trip per two
+        // depths; the same decisions as the one-node walk (ert.cpp:87-97)
+        auto px_of = [&](const SplitPlanes& q, bool second) {
+          const int an = second ? (short)(q.tail.z >> 16) : (short)(q.tail.z & 0xffff);
+          const double2 o = second ? q.ob : q.oa;
+          return sample_px<U8>(fr, w, h, pitch, X, Y, W, H, sc, ab.x, ab.y, an, o.x, o.y);
+        };
+        int d = 0;
+        for (; BL_ERT_SPEC2 && d + 2 <= M.F; d += 2) {
+          SplitPlanes r0, r1, r2;
+          rec_s(node, jl, r0);
+          rec_s(2 * node + 1, jl, r1);
+          rec_s(2 * node + 2, jl, r2);
+          const double i0a = px_of(r0, false), i0b = px_of(r0, true);
+          const double i1a = px_of(r1, false), i1b = px_of(r1, true);
+          const double i2a = px_of(r2, false), i2b = px_of(r2, true);
+          const bool right0 = dsub(i0a, i0b) > __hiloint2double(r0.tail.y, r0.tail.x);
+          const int c = right0 ? 2 * node + 1 : 2 * node + 2;
+          const SplitPlanes& rc = right0 ? r1 : r2;
+          const bool right1 = dsub(right0 ? i1a : i2a, right0 ? i1b : i2b) > __hiloint2double(rc.tail.y, rc.tail.x);
+          node = right1 ? 2 * c + 1 : 2 * c + 2;
+        }
+        for (; d < M.F; ++d) {
           rec_s(node, jl, r);
           const double thr = __hiloint2double(r.tail.y, r.tail.x);
           const int an_a = (short)(r.tail.z & 0xffff), an_b = (short)(r.tail.z >> 16);
