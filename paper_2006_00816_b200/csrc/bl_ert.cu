@@ -104,7 +104,11 @@ __global__ void __launch_bounds__(32 * kXfFaces) k_ert_xform(ErtDev M, const int
 //    order, then an xor butterfly over the 32 lanes (every lane ends with the same bits);
 //  * leaf sums: partial sums over chunks of kLeafChunk consecutive trees (each in tree order,
 //    from 0.0), then the partials in chunk order.
-constexpr int kLeafChunk = 64;
+#ifndef BL_LEAF_CHUNK
+#define BL_LEAF_CHUNK 64
+#endif
+constexpr int kLeafChunk = BL_LEAF_CHUNK;
+static_assert(kLeafChunk % 16 == 0, "16 leaf indices per 16-B load");
 
 BL_DEV double warp_sum(double v) {
 #pragma unroll
@@ -622,7 +626,7 @@ __global__ void __launch_bounds__(kWdMaxThreads, BL_WD_MINB) k_ert_wide(ErtDev M
 // update (partials in chunk order, ert.cpp:118-126) to its own copy of the shape; the
 // transform (warp 0) is computed redundantly and identically in each CTA.  Bit-identical to
 // k_ert_wide.
-constexpr int kWclMax = 8;
+constexpr int kWclMax = 16;
 #ifndef BL_ERT_SPEC2
 #define BL_ERT_SPEC2 1  // k_ert_wcl traversal: two depths per pixel round trip (speculative children;
                         // all 15 nodes at once measured slower: C1 0.289 vs 0.216 ms, stack use)
@@ -979,6 +983,7 @@ static cudaError_t launch_wcl(const Launch& L, const ErtDev& M, const void* fram
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (CL > 8) cudaFuncSetAttribute(k_ert_wcl<U8, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return cudaLaunchKernelEx(&cfg, k_ert_wcl<U8, CL>, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride,
                             n_faces, cap, out_xy, leaf_out, leaf_out_stride, err);
 }
@@ -989,7 +994,7 @@ void launch_ert_wide(const Launch& L, const ErtDev& M, const void* frames, int u
                      long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces,
                      int cap, double* out_xy, uint8_t* leaf_out, long long leaf_out_stride, int* err, int cl_req) {
   const int cl = cl_req;  // 1: one CTA per face; 2, 4, 8: a cluster of that many CTAs per face
-  if (cl == 2 || cl == 4 || cl == 8) {
+  if (cl == 2 || cl == 4 || cl == 8 || cl == 16) {
     cudaError_t r = cudaSuccess;
     if (cl == 2)
       r = u8 ? launch_wcl<true, 2>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err)
@@ -997,9 +1002,12 @@ void launch_ert_wide(const Launch& L, const ErtDev& M, const void* frames, int u
     else if (cl == 4)
       r = u8 ? launch_wcl<true, 4>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err)
              : launch_wcl<false, 4>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err);
-    else
+    else if (cl == 8)
       r = u8 ? launch_wcl<true, 8>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err)
              : launch_wcl<false, 8>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err);
+    else  // 16: a non-portable cluster size
+      r = u8 ? launch_wcl<true, 16>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err)
+             : launch_wcl<false, 16>(L, M, frames, w, h, pitch, fstride, face_frame, boxes, box_stride, n_faces, cap, out_xy, leaf_out, leaf_out_stride, err);
     (void)r;
     ++*L.counter;
     return;
@@ -1072,6 +1080,8 @@ void configure_ert_kernels(int optin) {  // per device, see configure_screen_tc_
   smem_optin(k_ert_wcl<false, 4>, optin);
   smem_optin(k_ert_wcl<true, 8>, optin);
   smem_optin(k_ert_wcl<false, 8>, optin);
+  smem_optin(k_ert_wcl<true, 16>, optin);
+  smem_optin(k_ert_wcl<false, 16>, optin);
 }
 
 }  // namespace blb

@@ -389,7 +389,7 @@ def test_ert_wide_and_cascade_kernels_agree(monkeypatch, oracle, n):
 
 @pytest.mark.parametrize("K", [40, 300, 500])
 def test_ert_cluster_sizes_agree(monkeypatch, oracle, K):
-    """The small-batch cascade as clusters of 2, 4 and 8 CTAs per face (k_ert_wcl: chunks
+    """The small-batch cascade as clusters of 2, 4, 8 and 16 (non-portable) CTAs per face (k_ert_wcl: chunks
     spread over the cluster, partials broadcast through DSMEM; 2 = unstaged sums, 4 = two
     chunks per CTA, 8 = one chunk per CTA and ranks without a chunk when K <= 448) is
     bit-identical to the one-CTA kernel and matches the oracle's leaves and landmarks."""
@@ -402,14 +402,14 @@ def test_ert_cluster_sizes_agree(monkeypatch, oracle, K):
     boxes = np.stack([r.integers(-20, 260, n), r.integers(-20, 180, n), r.integers(30, 160, n),
                       r.integers(30, 160, n)], axis=1).astype(np.int32)
     out = {}
-    for cl in (1, 2, 4, 8):
+    for cl in (1, 2, 4, 8, 16):
         monkeypatch.setenv("BL_ERT", "wide")
         monkeypatch.setenv("BL_ERT_CL", str(cl))
         c = bl.Context(0)
         c.upload_ert(ert)
         out[cl] = c.landmarks(img.astype(np.uint8), np.zeros(n, np.int32), boxes, want_leaves=True)
         c.close()
-    for cl in (2, 4, 8):
+    for cl in (2, 4, 8, 16):
         assert np.array_equal(out[cl][0], out[1][0]), cl
         assert np.array_equal(out[cl][1], out[1][1]), cl
     for i in range(n):
