@@ -533,6 +533,10 @@ int record_detect(bl_ctx* c, const void* in, int pix, int n, long long pitch, lo
         C.ry[k] = double(P.lh[k - 1]) / P.lh[k];
       }
     }
+    C.zero_u64 = P.n_cand.as<unsigned long long>();
+    C.zero_i32 = P.det_count.as<int>();
+    C.n_zero_i32 = n;
+    C.zero_flag = P.overflow.as<int>();
     if (const int e = launch_pyramid_chain(L, C, pix == BL_PIX_U8))
       return set_err(BL_ERR_CUDA, "pyramid chain launch failed: %s", cudaGetErrorString((cudaError_t)e));
   }
@@ -555,9 +559,11 @@ int record_detect(bl_ctx* c, const void* in, int pix, int n, long long pitch, lo
   stage_mark(c, BL_STAGE_GRADHIST);
   const PlanDesc* Pd = P.desc.as<PlanDesc>();
   const int ns = P.host.n_scored;
-  CK(cudaMemsetAsync(P.n_cand.p, 0, sizeof(unsigned long long), c->st));
-  CK(cudaMemsetAsync(P.det_count.p, 0, sizeof(int) * n, c->st));
-  CK(cudaMemsetAsync(P.overflow.p, 0, sizeof(int), c->st));
+  if (!chain) {  // (the one-launch chain zeroes them itself)
+    CK(cudaMemsetAsync(P.n_cand.p, 0, sizeof(unsigned long long), c->st));
+    CK(cudaMemsetAsync(P.det_count.p, 0, sizeof(int) * n, c->st));
+    CK(cudaMemsetAsync(P.overflow.p, 0, sizeof(int), c->st));
+  }
   if (ns > 0) {
     // fused gradient + histogram + energy (the gradient field stays on chip)
     int s1 = 0;

@@ -231,6 +231,12 @@ struct PyrChain {
   double* lv[kMaxLevels];  // level k >= 1: frame 0, pixel (0, 0)
   long long lpitch[kMaxLevels], lfstride[kMaxLevels];
   double rx[kMaxLevels], ry[kMaxLevels];  // step k: double(w_{k-1}) / w_k (image.cpp:136-137)
+  // the batch's detection counters, zeroed by the chain's first CTA (instead of three memset
+  // nodes ahead of the next kernels; nullptr: not zeroed here)
+  unsigned long long* zero_u64;
+  int* zero_i32;  // [n_zero_i32]
+  int n_zero_i32;
+  int* zero_flag;
 };
 int launch_pyramid_chain(const Launch& L, const PyrChain& C, int src_u8);
 void launch_resample_pair(const Launch& L, const void* src, int src_u8, int sw, int sh, long long s_pitch,

@@ -294,6 +294,13 @@ template <typename T0>
 __global__ void __launch_bounds__(256) k_pyramid_chain(const PyrChain C) {
   cg::grid_group grid = cg::this_grid();
   const long long stride = (long long)gridDim.x * blockDim.x;
+  if (blockIdx.x == 0 && C.zero_i32) {  // read by kernels after this one in the stream
+    for (int i = threadIdx.x; i < C.n_zero_i32; i += blockDim.x) C.zero_i32[i] = 0;
+    if (threadIdx.x == 0) {
+      *C.zero_u64 = 0ull;
+      *C.zero_flag = 0;
+    }
+  }
   for (int k = 1; k < C.n_levels; ++k) {
     const int sw = C.lw[k - 1], sh = C.lh[k - 1], dw = C.lw[k], dh = C.lh[k];
     const double rx = C.rx[k], ry = C.ry[k];
