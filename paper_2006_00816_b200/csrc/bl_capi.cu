@@ -655,7 +655,8 @@ int ert_work_ensure(const ErtState& E, ErtWork& wk, int nf, bool leaf_scratch) {
 
 int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix, int w, int h, long long pitch,
             long long fstride, const int* face_frame, const int* boxes, int box_stride, const int* n_faces_dev,
-            int nf, uint8_t* leaf_dev, double* out_xy, int* err_dev, long long expect_faces) {
+            int nf, uint8_t* leaf_dev, double* out_xy, int* err_dev, long long expect_faces,
+            bool err_zeroed = false) {
   ErtState& E = (*c->ertp);
   const Launch L{st, &c->launches};
   TRY(ert_work_ensure(E, wk, nf, leaf_dev == nullptr));
@@ -666,7 +667,7 @@ int run_ert(bl_ctx* c, cudaStream_t st, ErtWork& wk, const void* frames, int pix
     leaf_stride = div_up(E.dev.K, 16) * 16;  // 16-B aligned rows: 128-bit index loads
     leaf = wk.leafs.as<uint8_t>();
   }
-  CK(cudaMemsetAsync(err_dev, 0, sizeof(int), st));
+  if (!err_zeroed) CK(cudaMemsetAsync(err_dev, 0, sizeof(int), st));
   // one launch for the whole cascade: a face per CTA while the batch is too small to fill the
   // GPU with kFcFaces-face CTAs (latency), else kFcFaces faces per CTA (leaf-row reuse in L1)
   const bool wide = c->ert_mode == 2 || (c->ert_mode == 0 && expect_faces <= kErtWideMaxFaces);
@@ -876,8 +877,7 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
     launch_flatten(launch_of(c), P.kept.as<DevDet>(), P.kept_count.as<int>(), P.cap_pf, n, P.offsets.as<int>(),
                    S.flat.as<DevDet>(), S.face_frame.as<int>(), meta, cap_faces, P.overflow.as<int>(),
                    best_only ? S.best.as<DevDet>() : nullptr, best_only ? S.best_frame.as<int>() : nullptr);
-    if (!landmarks) CK(cudaMemsetAsync(meta + n + 2, 0, sizeof(int), c->st));
-    return BL_OK;
+    return BL_OK;  // (k_flatten zeroes meta[n + 2], the cascade's error flag)
   };
   if (graph) {
     bl_ctx::GraphEntry key;
@@ -914,10 +914,10 @@ int enqueue(bl_ctx* c, int s, const void* frames, int pix, int n, int w, int h, 
     auto rec_ert = [&](cudaStream_t st) -> int {
       if (best_only)  // the face of each frame only (run(), pipeline.cpp:171-190): row f = frame f
         return run_ert(c, st, S.ert, dev, pix, w, h, dp, df, S.best_frame.as<int>(), S.best.as<int>(), 8,
-                       meta + n + 3, n, nullptr, S.ert_out.as<double>(), meta + n + 2, n);
+                       meta + n + 3, n, nullptr, S.ert_out.as<double>(), meta + n + 2, n, true);
       return run_ert(c, st, S.ert, dev, pix, w, h, dp, df, S.face_frame.as<int>(), S.flat.as<int>(), 8, meta + n,
                      (int)cap_faces, nullptr, S.ert_out.as<double>(), meta + n + 2,
-                     (long long)n * kErtFacesPerFrameGuess);
+                     (long long)n * kErtFacesPerFrameGuess, true);
     };
     if (graph) {
       TRY(ert_work_ensure((*c->ertp), S.ert, (int)lm_rows, true));

@@ -811,6 +811,7 @@ __global__ void __launch_bounds__(1024) k_flatten(const DevDet* __restrict__ kep
     offsets[n_frames] = s_part[tid];
     meta[n_frames] = s_part[tid];
     meta[n_frames + 1] = *raw_overflow;
+    meta[n_frames + 2] = 0;  // the landmark cascade's error flag (the cascade runs after this kernel)
     meta[n_frames + 3] = n_frames;  // faces of the best-detection landmark list
   }
   if (best) {  // the face of every frame = its first kept detection (pipeline.cpp:167); a frame
