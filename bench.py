@@ -24,8 +24,8 @@ under torchrun it uses the launcher's ranks.
 
 `value` is device-resident throughput (frames already in HBM); `e2e` is the same metric
 through the public C-ABI call with pinned host frames (H2D of the frames and D2H of all
-detections + landmarks inside the timed region).  Each step's inputs (B*307 KB u8, 157 MB
-at B=512) exceed the 126 MB L2, so no explicit L2 flush is needed.  At N=1 the line also
+detections + landmarks inside the timed region).  Each step's inputs (B*307 KB u8, 315 MB
+at the default B=1024) exceed the 126 MB L2, so no explicit L2 flush is needed.  At N=1 the line also
 carries `configs`: the other BASELINE.json configurations (C1 single-frame latency, C2, C3,
 C5 throughput, C4 landmarks-only), each with its own e2e, roofline and CPU baseline.
 """
@@ -59,7 +59,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=40)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--batch", type=int, default=512, help="frames per GPU per step")
+    p.add_argument("--batch", type=int, default=1024, help="frames per GPU per step")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -448,7 +448,15 @@ def run_ours(args):
 
     configs = None
     if rank == 0 and world == 1 and not args.no_configs:
-        configs = measure_configs(args, torch, bl, ctx, stream, det, ert)
+        # a fresh context: the configs' own plans and pinned staging, not the bench batch's
+        # (the main context's ~20 GB of lane arenas and slot buffers are released first)
+        ctx.close()
+        cctx = bl.Context(local)
+        cctx.upload_detector(det)
+        cctx.upload_ert(ert)
+        cctx.set_stream(stream.cuda_stream)
+        configs = measure_configs(args, torch, bl, cctx, stream, det, ert)
+        cctx.close()
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "frames/s", "n_gpus": world, "steps": args.steps,

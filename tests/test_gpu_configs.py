@@ -116,14 +116,15 @@ def test_c5_1080p_full_batch256(ctx, oracle, pattern_model):
 
 
 def test_bench_workload_vs_oracle(ctx, oracle, pattern_model):
-    """bench.py's exact workload: 512 640x480 ring frames in one call with the 15 x 500 x
-    depth-4 cascade (seed 2020) on every kept detection; three frames against the oracle."""
-    frames = ring_frames_np(512, 640, 480, seed=1000)
+    """bench.py's exact workload: 1024 640x480 ring frames (its default batch) in one call
+    with the 15 x 500 x depth-4 cascade (seed 2020) on every kept detection; four frames
+    against the oracle."""
+    frames = ring_frames_np(1024, 640, 480, seed=1000)
     ert = random_ert(T=15, K=500, F=4, seed=2020)
     ctx.upload_detector(pattern_model)
     ctx.upload_ert(ert)
-    dets, lms, faces = _check_frames(ctx, oracle, pattern_model, ert, frames, [0, 257, 511])
-    assert faces > 0 and sum(len(d) for d in dets) > 512
+    dets, lms, faces = _check_frames(ctx, oracle, pattern_model, ert, frames, [0, 257, 700, 1023])
+    assert faces > 0 and sum(len(d) for d in dets) > 1024
 
 
 def test_bench_batch_vs_small_batch_kernels(ctx, pattern_model):
