@@ -128,7 +128,7 @@ def test_bench_workload_vs_oracle(ctx, oracle, pattern_model):
 
 
 def test_bench_batch_vs_small_batch_kernels(ctx, pattern_model):
-    """The bench's 512-frame batch runs 24-row gradHist segments and the 4-faces-per-CTA
+    """The bench's 512-frame batch runs tall (64-row) gradHist segments and the 4-faces-per-CTA
     cascade; a 3-frame batch of the same frames runs 1-row segments and the face-per-CTA
     cascade (k_ert_wide).  Both configurations give bit-identical detections and landmarks."""
     frames = ring_frames_np(512, 640, 480, seed=606)

@@ -1,4 +1,4 @@
-"""gradHist stage time at the bench batch (512 x 640x480 frames, device-resident), detection
+"""gradHist stage time at the bench batch (HOG_BATCH, default 1024 x 640x480 frames, device-resident), detection
 only, with a large face capacity so timing experiments that break results still run.
     BL_LIBRARY=... python tools/hog_time.py [reps]"""
 import os
@@ -16,7 +16,7 @@ det, ert = bench.load_models()
 ctx = bl.Context(0)
 ctx.upload_detector(det)
 ctx.set_face_capacity(4096)
-frames = torch.from_numpy(bench.frames_range(0, 512)).cuda()
+frames = torch.from_numpy(bench.frames_range(0, int(os.environ.get("HOG_BATCH", "1024")))).cuda()
 ctx.detect(frames, flat=True)
 ctx.enable_stage_timing(True)
 acc = {}
