@@ -30,6 +30,9 @@ constexpr bool kRsPairs = BL_RS_PAIRS;  // k_resample2 where the destination all
 #define BL_RS_COLS 2
 #endif
 constexpr int kRsCols = BL_RS_COLS;  // output columns per k_resample2 thread (2 or 4)
+#ifndef BL_RS_TALL
+#define BL_RS_TALL 8  // output rows per k_resample2 thread for large levels
+#endif
 
 template <typename Tin>
 __global__ void __launch_bounds__(256) k_resample(const Tin* __restrict__ src, int sw, int sh,
@@ -251,18 +254,18 @@ void launch_resample(const Launch& L, const void* src, int src_u8, int sw, int s
     // large levels (the bench's 512 frames): 8 output rows per thread (pyramid 1.27 -> 1.24 ms
     // per step); small ones keep 4 for more threads (C2's 16 frames: 0.040 vs 0.049 ms)
     const bool tall = (long long)n * dw * dh >= (8LL << 20);
-    const int rows = tall ? 8 : kRsRows;
+    const int rows = tall ? BL_RS_TALL : kRsRows;
     const dim3 grid2((unsigned)div_up(dw, 32 * kRsCols), (unsigned)div_up(dh, 8 * rows), (unsigned)n);
     if (src_u8) {
       if (tall)
-        k_resample2<uint8_t, kRsCols, 8><<<grid2, block, 0, L.st>>>((const uint8_t*)src, sw, sh, s_pitch, s_fstride,
+        k_resample2<uint8_t, kRsCols, BL_RS_TALL><<<grid2, block, 0, L.st>>>((const uint8_t*)src, sw, sh, s_pitch, s_fstride,
                                                                     dst, dw, dh, d_pitch, d_fstride, rx, ry);
       else
         k_resample2<uint8_t, kRsCols><<<grid2, block, 0, L.st>>>((const uint8_t*)src, sw, sh, s_pitch, s_fstride, dst,
                                                                  dw, dh, d_pitch, d_fstride, rx, ry);
     } else {
       if (tall)
-        k_resample2<double, kRsCols, 8><<<grid2, block, 0, L.st>>>((const double*)src, sw, sh, s_pitch, s_fstride,
+        k_resample2<double, kRsCols, BL_RS_TALL><<<grid2, block, 0, L.st>>>((const double*)src, sw, sh, s_pitch, s_fstride,
                                                                    dst, dw, dh, d_pitch, d_fstride, rx, ry);
       else
         k_resample2<double, kRsCols><<<grid2, block, 0, L.st>>>((const double*)src, sw, sh, s_pitch, s_fstride, dst,
