@@ -596,11 +596,6 @@ int record_detect(bl_ctx* c, const void* in, int pix, int n, long long pitch, lo
   return BL_OK;
 }
 
-int run_detect(bl_ctx* c, const void* in, int pix, int n, int w, int h, long long pitch, long long fstride) {
-  TRY(prepare_detect(c, pix, n, w, h, pitch, fstride));
-  return record_detect(c, in, pix, n, pitch, fstride);
-}
-
 // Stage host frames into a device buffer (or use device frames in place).
 int stage_input(bl_ctx* c, DevBuf& buf, const void* frames, int pix, int n, int w, int h, size_t pitch,
                 size_t fstride, const void** dev, long long* dpitch, long long* dfstride) {

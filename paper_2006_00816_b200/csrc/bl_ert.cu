@@ -626,7 +626,6 @@ __global__ void __launch_bounds__(kWdMaxThreads, BL_WD_MINB) k_ert_wide(ErtDev M
 // update (partials in chunk order, ert.cpp:118-126) to its own copy of the shape; the
 // transform (warp 0) is computed redundantly and identically in each CTA.  Bit-identical to
 // k_ert_wide.
-constexpr int kWclMax = 16;
 #ifndef BL_ERT_SPEC2
 #define BL_ERT_SPEC2 1  // k_ert_wcl traversal: two depths per pixel round trip (speculative children;
                         // all 15 nodes at once measured slower: C1 0.289 vs 0.216 ms, stack use)
